@@ -1,0 +1,142 @@
+/*
+ * dgmg_b200.h - C ABI of the B200-native Schwarz-smoother hot path.
+ *
+ * Drop-in boundary for the reference package `dgmg` (arXiv 1910.11239,
+ * /root/reference/pkg/src/dgmg).  The reference is pure Python; its hot path
+ * is the fp64 Schwarz smoothing step on a uniform Cartesian SIPG level:
+ *
+ *   residual r = b - A x          dgop.residual        dgop.py:782-788
+ *   operator v = A u              dgop.apply_operator  dgop.py:762-779
+ *   cell FDM solves               CellSolverSet.solve_partitioned   fastdiag.py:457-496
+ *   patch FDM solves              PatchSolverSet.solve_partitioned  fastdiag.py:602-628
+ *   additive / multiplicative     LevelSmoother.smooth_additive / _multiplicative
+ *                                 smoothers.py:131-166
+ *
+ * The Python mirror (paper_1910_11239_b200/) keeps those entry points and
+ * binds the functions below through ctypes.
+ *
+ * Conventions
+ *  - all vectors are device fp64 in the reference's canonical layout
+ *    (cell-major, dof = cell*n^d + sum_t i_t n^(t-1), dgop.py:70-103);
+ *  - every compute call is asynchronous on the caller's stream and returns
+ *    DG_OK or an error code; dg_last_error() gives the thread-local message;
+ *  - a level may hold a window of cell layers along the last direction
+ *    (slab decomposition across GPUs): layers [z_begin, z_begin+z_count) of a
+ *    global box with ncells[t] cells per direction are stored contiguously.
+ */
+#ifndef DGMG_B200_H
+#define DGMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DG_OK = 0,
+  DG_EINVAL = 1,      /* bad size / alias / argument  -> ValueError            */
+  DG_ESINGULAR = 2,   /* nonpositive Kronecker eigenvalue sum (fastdiag.py:98) */
+  DG_ECUDA = 3,       /* CUDA runtime failure                                  */
+  DG_EUNSUPPORTED = 4 /* (dim, degree) without a compiled kernel               */
+};
+
+/* smoother kinds, SmootherConfig.kind (smoothers.py:41-69) */
+enum { DG_ACS = 0, DG_MCS = 1, DG_AVS = 2, DG_MVS = 3 };
+
+typedef struct dg_level_desc {
+  int dim;            /* 2 or 3                                                */
+  int degree;         /* k >= 1; n = k+1 nodes per direction                   */
+  int ncells[3];      /* global cells per direction (unused entries = 1)       */
+  int z_begin;        /* first stored layer along direction `dim`              */
+  int z_count;        /* stored layers                                         */
+  int own_begin;      /* owned layers [own_begin, own_end): cell solves/writes */
+  int own_end;
+  int res_begin;      /* layers whose residual dg_smooth computes              */
+  int res_end;
+  int pv_begin;       /* patch vertices v_dim in [pv_begin, pv_end] are solved */
+  int pv_end;
+} dg_level_desc_t;
+
+/* Host tables from the 1D setup (paper_1910_11239_b200/tables.py).  All
+ * matrices are row-major and applied as out_i = sum_k S[i*s+k] in_k.
+ * `digit` (0..3) encodes the boundary pattern of one direction: bit 0 = left
+ * face on the boundary, bit 1 = right face (fastdiag.py:349-369, 535-566).  */
+typedef struct dg_tables {
+  const double* mass;          /* n*n      1D cell mass M                      */
+  const double* adiag;         /* 4*n*n    1D cell stiffness per digit         */
+  const double* bg;            /* 2*n      basis derivatives at x=0, x=1       */
+  double alpha;                /* -gamma_e/2  (rank-2 face coupling a_pm)      */
+  double beta;                 /* -1/(2h)                                      */
+  double betap;                /* +1/(2h)                                      */
+  const double* cell_z;        /* 4*n*n    cell eigenvectors Z per digit       */
+  const double* cell_zt;       /* 4*n*n    Z^T                                 */
+  const double* cell_invsum;   /* 4^d*n^d  1/Lambda-sum per class, canonical   */
+  const double* patch_z;       /* 4*m*m    patch eigenvectors, m = 2n (or NULL)*/
+  const double* patch_zt;      /* 4*m*m                                        */
+  const double* patch_invsum;  /* 4^d*m^d                                      */
+} dg_tables_t;
+
+typedef struct dg_level dg_level_t;
+
+const char* dg_last_error(void);
+int dg_version(void);
+
+/* Level lifetime: uploads the tables, builds the colour lists (red-black
+ * cells, structured patch colours mesh.py:350-375) for the window.          */
+int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* tables,
+                    dg_level_t** out);
+int dg_level_destroy(dg_level_t* lvl);
+
+/* number of local dofs stored by the level (z_count layers)                 */
+int64_t dg_level_ndofs(const dg_level_t* lvl);
+
+/* v = A u on the cells of global layers [z0, z1) (dgop.apply_operator);
+ * u, v are local vectors, v must not alias u.                               */
+int dg_apply(const dg_level_t* lvl, const double* u, double* v,
+             int z0, int z1, void* stream);
+/* r = b - A x on the cells of layers [z0, z1) (dgop.residual)              */
+int dg_residual(const dg_level_t* lvl, const double* x, const double* b,
+                double* r, int z0, int z1, void* stream);
+/* r = b - A x on an explicit list of local cell ids (device int32)         */
+int dg_residual_cells(const dg_level_t* lvl, const double* x, const double* b,
+                      double* r, const int32_t* cells, int64_t n_cells,
+                      void* stream);
+
+/* x[cell dofs] += omega * A_c^{-1} r_c for local cell ids (device int32), or
+ * for all owned cells when cells == NULL (CellSolverSet.solve_partitioned). */
+int dg_cell_fdm(const dg_level_t* lvl, const double* r, double* x,
+                double omega, const int32_t* cells, int64_t n_cells,
+                void* stream);
+/* x[patch dofs] += omega * A_j^{-1} R_j r for global patch ids (device
+ * int32).  atomic != 0 accumulates with fp64 atomics (overlapping patches,
+ * safe_accumulate=True); otherwise the patches must be write-disjoint.     */
+int dg_patch_fdm(const dg_level_t* lvl, const double* r, double* x,
+                 double omega, const int32_t* patches, int64_t n_patches,
+                 int atomic, void* stream);
+
+/* colour lists built at create time (device int32, owned by the level)     */
+int dg_num_colours(const dg_level_t* lvl, int kind);
+int dg_colour_list(const dg_level_t* lvl, int kind, int colour,
+                   const int32_t** dev_ids, int64_t* count);
+/* R_j gather map of patches [first, first+count) as local dof indices
+ * (device int64, count*m^d), computed by the kernels' own index math.      */
+int dg_patch_gather_map(const dg_level_t* lvl, const int32_t* patches,
+                        int64_t count, int64_t* out, void* stream);
+
+/* One smoothing step / sweep (LevelSmoother.smooth, smoothers.py:131-166):
+ * ACS/AVS additive, MCS/MVS multiplicative (reverse flips colour order).
+ * scratch_r holds the residual (local size).  The launch sequence is
+ * captured once into a CUDA graph per (kind, omega, reverse, pointers) and
+ * replayed when use_graph != 0.                                             */
+int dg_smooth(dg_level_t* lvl, int kind, double omega, int reverse,
+              double* x, const double* b, double* scratch_r, int use_graph,
+              void* stream);
+
+/* kernels launched by the last dg_smooth call (for the bench's count)      */
+int64_t dg_last_launch_count(const dg_level_t* lvl);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGMG_B200_H */

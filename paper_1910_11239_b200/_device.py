@@ -1,0 +1,65 @@
+"""Device plumbing: torch for memory and streams, nothing else.
+
+The public API accepts numpy arrays (copied host<->device around the call, so
+that callers written for the reference, e.g. its V-cycle, work unchanged) and
+torch float64 CUDA tensors (zero-copy, ordered on the current stream).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+def require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1910_11239_b200 needs a CUDA device (no CPU fallback)")
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def is_device(a) -> bool:
+    return isinstance(a, torch.Tensor) and a.is_cuda
+
+
+class Staged:
+    """A device view of a caller vector; `finish()` writes back host arrays."""
+
+    __slots__ = ("host", "dev")
+
+    def __init__(self, a, ndofs: int, name: str, need_copy: bool = True,
+                 staging: torch.Tensor | None = None):
+        if isinstance(a, torch.Tensor):
+            if not a.is_cuda:
+                raise ValueError(f"{name}: torch tensors must live on a CUDA device")
+            if a.dtype != torch.float64:
+                raise ValueError(f"{name}: expected float64")
+            if a.numel() != ndofs:
+                raise ValueError(f"{name}: vector size does not match level")
+            if not a.is_contiguous():
+                raise ValueError(f"{name}: tensor must be contiguous")
+            self.host = None
+            self.dev = a.view(-1)
+            return
+        arr = np.asarray(a)
+        if arr.size != ndofs:
+            raise ValueError(f"{name}: vector size does not match level")
+        self.host = arr
+        if staging is None:
+            staging = torch.empty(ndofs, dtype=torch.float64, device="cuda")
+        if need_copy:
+            src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64).reshape(-1))
+            staging.copy_(src, non_blocking=False)
+        self.dev = staging
+
+    @property
+    def ptr(self) -> int:
+        return self.dev.data_ptr()
+
+    def finish(self) -> None:
+        if self.host is not None:
+            out = self.dev.cpu().numpy()
+            if self.host.flags.writeable:
+                np.copyto(self.host.reshape(-1), out)

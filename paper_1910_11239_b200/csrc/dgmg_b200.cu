@@ -1,0 +1,602 @@
+// dgmg_b200.cu - C ABI (include/dgmg_b200.h) over the sm_100a kernels.
+//
+// Host runtime responsibilities (native, C++):
+//  - level objects: device tables (one allocation), window geometry;
+//  - colour lists built in closed form: red-black cells (mesh.py:350-357),
+//    structured patch colours (mesh.py:360-375) in ascending colour order,
+//    patch ids ascending inside a colour, and per patch colour the cells the
+//    colour covers (the restricted MVS residual, SURVEY 8(d) kappa);
+//  - the smoothing-step launch sequences of LevelSmoother (smoothers.py:
+//    131-166), captured once into CUDA graphs and replayed.
+#include "../../include/dgmg_b200.h"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+namespace dgb {
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define DG_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      return fail(DG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+__global__ void gather_map_kernel(MapParams p) {
+  const int64_t per = (p.d == 3) ? (int64_t)p.m * p.m * p.m : (int64_t)p.m * p.m;
+  const int64_t total = p.count * per;
+  const int NEc = (p.d == 3) ? p.n * p.n * p.n : p.n * p.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t / per;
+    const int e = (int)(t % per);
+    int rem = p.list[k];
+    int c[3] = {0, 0, 0}, q[3] = {e % p.m, (e / p.m) % p.m, e / (p.m * p.m)};
+    int off = 0, mul = 1;
+    for (int s = 0; s < p.d; ++s) {
+      const int span = p.geo.nc[s] - 1;
+      const int v = 1 + rem % span;
+      rem /= span;
+      c[s] = v - 1 + q[s] / p.n;
+      off += (q[s] % p.n) * mul;
+      mul *= p.n;
+    }
+    int64_t cell;
+    if (p.d == 2) cell = c[0] + (int64_t)p.geo.nc[0] * (c[1] - p.geo.zb);
+    else cell = c[0] + (int64_t)p.geo.nc[0] * (c[1] + (int64_t)p.geo.nc[1] * (c[2] - p.geo.zb));
+    p.out[t] = cell * NEc + off;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// template dispatch
+// ---------------------------------------------------------------------------
+template <int D, int N>
+static int launch_residual(const ResParams& p, cudaStream_t st) {
+  if (p.count <= 0) return DG_OK;
+  constexpr int G = groups_for(Lay<D, N>::F);
+  const size_t smem = sizeof(double) * res_smem_doubles<D, N>();
+  auto k = residual_kernel<D, N>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int64_t grid = (p.count + G - 1) / G;
+  k<<<(unsigned)grid, G * Lay<D, N>::F, smem, st>>>(p);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
+template <int D, int M, bool PATCH>
+static int launch_fdm(const FdmParams& p, cudaStream_t st) {
+  if (p.count <= 0) return DG_OK;
+  constexpr int G = groups_for(Lay<D, M>::F);
+  const size_t smem = sizeof(double) * fdm_smem_doubles<D, M>();
+  auto k = fdm_kernel<D, M, PATCH>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int64_t grid = (p.count + G - 1) / G;
+  k<<<(unsigned)grid, G * Lay<D, M>::F, smem, st>>>(p);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
+#define DG_N_CASES(X, D) \
+  X(D, 2) X(D, 3) X(D, 4) X(D, 5) X(D, 6) X(D, 7) X(D, 8) X(D, 9) X(D, 10) \
+  X(D, 11) X(D, 12) X(D, 13) X(D, 14) X(D, 15) X(D, 16)
+
+static int dispatch_residual(int d, int n, const ResParams& p, cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_residual<D, N>(p, st);
+  DG_N_CASES(X, 2)
+  DG_N_CASES(X, 3)
+#undef X
+  return fail(DG_EUNSUPPORTED, "residual: no kernel for dim " + std::to_string(d) +
+                                   ", n " + std::to_string(n));
+}
+
+static int dispatch_cell_fdm(int d, int n, const FdmParams& p, cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_fdm<D, N, false>(p, st);
+  DG_N_CASES(X, 2)
+  DG_N_CASES(X, 3)
+#undef X
+  return fail(DG_EUNSUPPORTED, "cell fdm: no kernel for dim " + std::to_string(d) +
+                                   ", n " + std::to_string(n));
+}
+
+static int dispatch_patch_fdm(int d, int n, const FdmParams& p, cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_fdm<D, 2 * N, true>(p, st);
+  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
+  X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 6) X(3, 7) X(3, 8)
+#undef X
+  return fail(DG_EUNSUPPORTED, "patch fdm: no kernel for dim " + std::to_string(d) +
+                                   ", degree " + std::to_string(n - 1) +
+                                   " (vertex patches support k <= 7)");
+}
+
+}  // namespace dgb
+
+using namespace dgb;
+
+struct DevList {
+  int32_t* ptr = nullptr;
+  int64_t count = 0;
+};
+
+struct GraphKey {
+  int kind;
+  double omega;
+  int reverse;
+  const void* x;
+  const void* b;
+  const void* r;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(kind, omega, reverse, x, b, r) <
+           std::tie(o.kind, o.omega, o.reverse, o.x, o.b, o.r);
+  }
+};
+
+struct dg_level {
+  dg_level_desc_t desc;
+  int d = 0, n = 0, m = 0;
+  int64_t layer_cells = 0, ncells_local = 0, ndofs = 0, cell_dofs = 0;
+  Geo geo;
+  double* dtab = nullptr;
+  const double *mass = nullptr, *adiag = nullptr, *bg = nullptr;
+  const double *cz = nullptr, *czt = nullptr, *cinv = nullptr;
+  const double *pz = nullptr, *pzt = nullptr, *pinv = nullptr;
+  double alpha = 0, beta = 0, betap = 0;
+  bool has_patch = false;
+  std::vector<DevList> rb;          // red-black owned cells (MCS)
+  std::vector<DevList> pcol;        // patch colours (AVS / MVS)
+  std::vector<DevList> pcol_cells;  // cells covered by a patch colour (MVS)
+  cudaStream_t cap = nullptr;       // capture stream
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  int64_t last_launches = 0;
+};
+
+static int upload_list(const std::vector<int32_t>& h, DevList* out) {
+  out->count = (int64_t)h.size();
+  if (h.empty()) return DG_OK;
+  DG_CUDA(cudaMalloc(&out->ptr, h.size() * sizeof(int32_t)));
+  DG_CUDA(cudaMemcpy(out->ptr, h.data(), h.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  return DG_OK;
+}
+
+static void free_level(dg_level* L) {
+  if (!L) return;
+  for (auto& kv : L->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto* v : {&L->rb, &L->pcol, &L->pcol_cells})
+    for (auto& l : *v) cudaFree(l.ptr);
+  cudaFree(L->dtab);
+  if (L->cap) cudaStreamDestroy(L->cap);
+  delete L;
+}
+
+static ResParams res_params(const dg_level* L, const double* x, const double* b, double* r) {
+  ResParams p{};
+  p.x = x;
+  p.b = b;
+  p.r = r;
+  p.mass = L->mass;
+  p.adiag = L->adiag;
+  p.bg = L->bg;
+  p.alpha = L->alpha;
+  p.beta = L->beta;
+  p.betap = L->betap;
+  p.geo = L->geo;
+  return p;
+}
+
+static FdmParams fdm_params(const dg_level* L, bool patch, const double* r, double* x,
+                            double omega) {
+  FdmParams p{};
+  p.r = r;
+  p.x = x;
+  p.z = patch ? L->pz : L->cz;
+  p.zt = patch ? L->pzt : L->czt;
+  p.invsum = patch ? L->pinv : L->cinv;
+  p.omega = omega;
+  p.geo = L->geo;
+  return p;
+}
+
+static int check_layers(const dg_level* L, int z0, int z1) {
+  const int lo = L->desc.z_begin, hi = L->desc.z_begin + L->desc.z_count;
+  const int last = L->desc.ncells[L->d - 1];
+  if (z0 < lo || z1 > hi || z0 > z1)
+    return fail(DG_EINVAL, "layer range outside the stored window");
+  // neighbours of computed layers must be stored (or be the physical boundary)
+  if ((z0 > 0 && z0 - 1 < lo && z0 < z1) || (z1 < last && z1 >= hi && z0 < z1))
+    return fail(DG_EINVAL, "residual layers need a stored neighbour layer on each side");
+  return DG_OK;
+}
+
+extern "C" {
+
+const char* dg_last_error(void) { return g_err.c_str(); }
+
+int dg_version(void) { return 1; }
+
+int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_t** out) {
+  if (!desc || !T || !out) return fail(DG_EINVAL, "null argument");
+  *out = nullptr;
+  const int d = desc->dim;
+  if (d != 2 && d != 3) return fail(DG_EUNSUPPORTED, "device path supports dim 2 and 3");
+  const int n = desc->degree + 1;
+  if (desc->degree < 1 || n > 16)
+    return fail(DG_EUNSUPPORTED, "device path supports 1 <= degree <= 15");
+  for (int t = 0; t < d; ++t)
+    if (desc->ncells[t] < 1) return fail(DG_EINVAL, "ncells must be >= 1");
+  const int last = desc->ncells[d - 1];
+  if (desc->z_begin < 0 || desc->z_count < 1 || desc->z_begin + desc->z_count > last)
+    return fail(DG_EINVAL, "stored window outside the level");
+  auto* L = new dg_level();
+  L->desc = *desc;
+  L->d = d;
+  L->n = n;
+  L->m = 2 * n;
+  L->layer_cells = (d == 3) ? (int64_t)desc->ncells[0] * desc->ncells[1] : desc->ncells[0];
+  L->ncells_local = L->layer_cells * desc->z_count;
+  L->cell_dofs = (d == 3) ? (int64_t)n * n * n : (int64_t)n * n;
+  L->ndofs = L->ncells_local * L->cell_dofs;
+  L->geo.nc[0] = desc->ncells[0];
+  L->geo.nc[1] = d >= 2 ? desc->ncells[1] : 1;
+  L->geo.nc[2] = d == 3 ? desc->ncells[2] : 1;
+  L->geo.zb = desc->z_begin;
+  L->geo.zn = desc->z_count;
+  L->alpha = T->alpha;
+  L->beta = T->beta;
+  L->betap = T->betap;
+  L->has_patch = T->patch_z != nullptr && n <= 8;
+  const int m = L->m;
+  const int64_t pw = (d == 3) ? 64 : 16;  // 4^d classes
+  const int64_t ce = L->cell_dofs, pe = (d == 3) ? (int64_t)m * m * m : (int64_t)m * m;
+  std::vector<std::pair<const double*, int64_t>> parts = {
+      {T->mass, n * n},  {T->adiag, 4 * n * n}, {T->bg, 2 * n},
+      {T->cell_z, 4 * n * n}, {T->cell_zt, 4 * n * n}, {T->cell_invsum, pw * ce}};
+  if (L->has_patch) {
+    parts.push_back({T->patch_z, 4 * m * m});
+    parts.push_back({T->patch_zt, 4 * m * m});
+    parts.push_back({T->patch_invsum, pw * pe});
+  }
+  int64_t total = 0;
+  for (auto& pr : parts) total += (pr.second + 1) & ~int64_t(1);
+  cudaError_t e = cudaMalloc(&L->dtab, total * sizeof(double));
+  if (e != cudaSuccess) {
+    free_level(L);
+    return fail(DG_ECUDA, std::string("cudaMalloc tables: ") + cudaGetErrorString(e));
+  }
+  std::vector<const double*> dptr;
+  int64_t off = 0;
+  for (auto& pr : parts) {
+    if (!pr.first) {
+      free_level(L);
+      return fail(DG_EINVAL, "missing table");
+    }
+    e = cudaMemcpy(L->dtab + off, pr.first, pr.second * sizeof(double), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      free_level(L);
+      return fail(DG_ECUDA, std::string("cudaMemcpy tables: ") + cudaGetErrorString(e));
+    }
+    dptr.push_back(L->dtab + off);
+    off += (pr.second + 1) & ~int64_t(1);
+  }
+  L->mass = dptr[0];
+  L->adiag = dptr[1];
+  L->bg = dptr[2];
+  L->cz = dptr[3];
+  L->czt = dptr[4];
+  L->cinv = dptr[5];
+  if (L->has_patch) {
+    L->pz = dptr[6];
+    L->pzt = dptr[7];
+    L->pinv = dptr[8];
+  }
+
+  // ---- colour lists -------------------------------------------------------
+  const int* nc = desc->ncells;
+  const int zb = desc->z_begin;
+  auto local_of = [&](const int* c) -> int32_t {
+    if (d == 2) return (int32_t)(c[0] + (int64_t)nc[0] * (c[1] - zb));
+    return (int32_t)(c[0] + (int64_t)nc[0] * (c[1] + (int64_t)nc[1] * (c[2] - zb)));
+  };
+  // red-black over owned cells (mesh.py:350-357), ascending local ids
+  {
+    std::vector<int32_t> col[2];
+    const int64_t c0 = (int64_t)(desc->own_begin - zb) * L->layer_cells;
+    const int64_t c1 = (int64_t)(desc->own_end - zb) * L->layer_cells;
+    for (int64_t id = c0; id < c1; ++id) {
+      int64_t rem = id;
+      int s = 0;
+      for (int t = 0; t < d; ++t) {
+        const int64_t ct = (t == d - 1) ? rem + zb : rem % nc[t];
+        rem /= nc[t];
+        s += (int)ct;
+      }
+      col[s & 1].push_back((int32_t)id);
+    }
+    for (int k = 0; k < 2; ++k) {
+      if (col[k].empty()) continue;
+      DevList dl;
+      int rc = upload_list(col[k], &dl);
+      L->rb.push_back(dl);
+      if (rc) { free_level(L); return rc; }
+    }
+  }
+  // structured patch colours (mesh.py:360-375) for vertices v_d in
+  // [pv_begin, pv_end]; ids ascending inside each colour
+  if (L->has_patch) {
+    const int ncol = 1 << (d + 1);
+    std::vector<std::vector<int32_t>> pc(ncol), cc(ncol);
+    bool ok = true;
+    for (int t = 0; t < d; ++t) ok = ok && nc[t] >= 2;
+    const int vlo = std::max(1, desc->pv_begin), vhi = std::min(nc[d - 1] - 1, desc->pv_end);
+    if (ok && vlo <= vhi) {
+      if (vlo - 1 < zb || vhi > zb + desc->z_count - 1) {
+        free_level(L);
+        return fail(DG_EINVAL, "patch vertex range needs cell layers outside the window");
+      }
+      int64_t layer_patches = 1;
+      for (int t = 0; t < d - 1; ++t) layer_patches *= (nc[t] - 1);
+      const int64_t p0 = (int64_t)(vlo - 1) * layer_patches, p1 = (int64_t)vhi * layer_patches;
+      for (int64_t id = p0; id < p1; ++id) {
+        int64_t rem = id;
+        int v[3] = {1, 1, 1}, parq = 0, half = 0;
+        for (int t = 0; t < d; ++t) {
+          v[t] = 1 + (int)(rem % (nc[t] - 1));
+          rem /= (nc[t] - 1);
+          parq += (v[t] & 1) << t;
+          half += v[t] / 2;
+        }
+        const int col = parq * 2 + (half & 1);
+        pc[col].push_back((int32_t)id);
+        for (int s = 0; s < (1 << d); ++s) {
+          int c[3] = {0, 0, 0};
+          for (int t = 0; t < d; ++t) c[t] = v[t] - 1 + ((s >> t) & 1);
+          cc[col].push_back(local_of(c));
+        }
+      }
+    }
+    for (int k = 0; k < ncol; ++k) {
+      if (pc[k].empty()) continue;
+      DevList a, b;
+      int rc = upload_list(pc[k], &a);
+      L->pcol.push_back(a);
+      if (!rc) rc = upload_list(cc[k], &b);
+      L->pcol_cells.push_back(b);
+      if (rc) { free_level(L); return rc; }
+    }
+  }
+  if (desc->own_begin < zb || desc->own_end > zb + desc->z_count ||
+      desc->own_begin > desc->own_end) {
+    free_level(L);
+    return fail(DG_EINVAL, "owned layers outside the window");
+  }
+  if (int rc = check_layers(L, desc->res_begin, desc->res_end)) {
+    free_level(L);
+    return rc;
+  }
+  e = cudaStreamCreateWithFlags(&L->cap, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    free_level(L);
+    return fail(DG_ECUDA, std::string("stream create: ") + cudaGetErrorString(e));
+  }
+  *out = L;
+  return DG_OK;
+}
+
+int dg_level_destroy(dg_level_t* L) {
+  free_level(L);
+  return DG_OK;
+}
+
+int64_t dg_level_ndofs(const dg_level_t* L) { return L ? L->ndofs : -1; }
+
+int dg_apply(const dg_level_t* L, const double* u, double* v, int z0, int z1, void* stream) {
+  if (!L || !u || !v) return fail(DG_EINVAL, "null argument");
+  if (u == v) return fail(DG_EINVAL, "apply_operator: output must not alias input");
+  if (int rc = check_layers(L, z0, z1)) return rc;
+  ResParams p = res_params(L, u, nullptr, v);
+  p.start = (int64_t)(z0 - L->desc.z_begin) * L->layer_cells;
+  p.count = (int64_t)(z1 - z0) * L->layer_cells;
+  return dispatch_residual(L->d, L->n, p, (cudaStream_t)stream);
+}
+
+int dg_residual(const dg_level_t* L, const double* x, const double* b, double* r, int z0,
+                int z1, void* stream) {
+  if (!L || !x || !b || !r) return fail(DG_EINVAL, "null argument");
+  if (r == x) return fail(DG_EINVAL, "residual: output must not alias x");
+  if (int rc = check_layers(L, z0, z1)) return rc;
+  ResParams p = res_params(L, x, b, r);
+  p.start = (int64_t)(z0 - L->desc.z_begin) * L->layer_cells;
+  p.count = (int64_t)(z1 - z0) * L->layer_cells;
+  return dispatch_residual(L->d, L->n, p, (cudaStream_t)stream);
+}
+
+int dg_residual_cells(const dg_level_t* L, const double* x, const double* b, double* r,
+                      const int32_t* cells, int64_t n_cells, void* stream) {
+  if (!L || !x || !b || !r || (!cells && n_cells > 0)) return fail(DG_EINVAL, "null argument");
+  if (r == x) return fail(DG_EINVAL, "residual: output must not alias x");
+  ResParams p = res_params(L, x, b, r);
+  p.list = cells;
+  p.count = n_cells;
+  return dispatch_residual(L->d, L->n, p, (cudaStream_t)stream);
+}
+
+int dg_cell_fdm(const dg_level_t* L, const double* r, double* x, double omega,
+                const int32_t* cells, int64_t n_cells, void* stream) {
+  if (!L || !r || !x) return fail(DG_EINVAL, "null argument");
+  if (r == x) return fail(DG_EINVAL, "cell solve: r must not alias x");
+  FdmParams p = fdm_params(L, false, r, x, omega);
+  if (cells) {
+    p.list = cells;
+    p.count = n_cells;
+  } else {
+    p.start = (int64_t)(L->desc.own_begin - L->desc.z_begin) * L->layer_cells;
+    p.count = (int64_t)(L->desc.own_end - L->desc.own_begin) * L->layer_cells;
+  }
+  return dispatch_cell_fdm(L->d, L->n, p, (cudaStream_t)stream);
+}
+
+int dg_patch_fdm(const dg_level_t* L, const double* r, double* x, double omega,
+                 const int32_t* patches, int64_t n_patches, int atomic, void* stream) {
+  if (!L || !r || !x || (!patches && n_patches > 0)) return fail(DG_EINVAL, "null argument");
+  if (r == x) return fail(DG_EINVAL, "patch solve: r must not alias x");
+  if (!L->has_patch)
+    return fail(DG_EUNSUPPORTED, "vertex-patch tables not available (degree > 7?)");
+  FdmParams p = fdm_params(L, true, r, x, omega);
+  p.list = patches;
+  p.count = n_patches;
+  p.atomic = atomic;
+  return dispatch_patch_fdm(L->d, L->n, p, (cudaStream_t)stream);
+}
+
+int dg_num_colours(const dg_level_t* L, int kind) {
+  if (!L) return -1;
+  switch (kind) {
+    case DG_ACS: return 1;
+    case DG_MCS: return (int)L->rb.size();
+    case DG_AVS:
+    case DG_MVS: return (int)L->pcol.size();
+  }
+  return -1;
+}
+
+int dg_colour_list(const dg_level_t* L, int kind, int colour, const int32_t** ids,
+                   int64_t* count) {
+  if (!L || !ids || !count) return fail(DG_EINVAL, "null argument");
+  const std::vector<DevList>* v = nullptr;
+  if (kind == DG_MCS) v = &L->rb;
+  else if (kind == DG_AVS || kind == DG_MVS) v = &L->pcol;
+  else if (kind == 100) v = &L->pcol_cells;
+  if (!v || colour < 0 || colour >= (int)v->size()) return fail(DG_EINVAL, "no such colour");
+  *ids = (*v)[colour].ptr;
+  *count = (*v)[colour].count;
+  return DG_OK;
+}
+
+int dg_patch_gather_map(const dg_level_t* L, const int32_t* patches, int64_t count,
+                        int64_t* out, void* stream) {
+  if (!L || (!patches && count > 0) || (!out && count > 0)) return fail(DG_EINVAL, "null argument");
+  if (count <= 0) return DG_OK;
+  MapParams p{};
+  p.list = patches;
+  p.count = count;
+  p.out = out;
+  p.m = L->m;
+  p.n = L->n;
+  p.d = L->d;
+  p.geo = L->geo;
+  gather_map_kernel<<<1024, 256, 0, (cudaStream_t)stream>>>(p);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
+static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, double* x,
+                           const double* b, double* r, cudaStream_t st, int64_t* nl) {
+  int rc = DG_OK;
+  *nl = 0;
+  auto res_range = [&]() {
+    ResParams p = res_params(L, x, b, r);
+    p.start = (int64_t)(L->desc.res_begin - L->desc.z_begin) * L->layer_cells;
+    p.count = (int64_t)(L->desc.res_end - L->desc.res_begin) * L->layer_cells;
+    ++*nl;
+    return dispatch_residual(L->d, L->n, p, st);
+  };
+  switch (kind) {
+    case DG_ACS: {
+      if ((rc = res_range())) return rc;
+      ++*nl;
+      return dg_cell_fdm(L, r, x, omega, nullptr, 0, st);
+    }
+    case DG_AVS: {
+      if (!L->has_patch) return fail(DG_EUNSUPPORTED, "vertex patches unsupported here");
+      if ((rc = res_range())) return rc;
+      for (auto& c : L->pcol) {
+        ++*nl;
+        if ((rc = dg_patch_fdm(L, r, x, omega, c.ptr, c.count, 0, st))) return rc;
+      }
+      return DG_OK;
+    }
+    case DG_MCS: {
+      const int nc = (int)L->rb.size();
+      for (int i = 0; i < nc; ++i) {
+        const auto& c = L->rb[reverse ? nc - 1 - i : i];
+        *nl += 2;
+        if ((rc = dg_residual_cells(L, x, b, r, c.ptr, c.count, st))) return rc;
+        if ((rc = dg_cell_fdm(L, r, x, omega, c.ptr, c.count, st))) return rc;
+      }
+      return DG_OK;
+    }
+    case DG_MVS: {
+      if (!L->has_patch) return fail(DG_EUNSUPPORTED, "vertex patches unsupported here");
+      const int nc = (int)L->pcol.size();
+      for (int i = 0; i < nc; ++i) {
+        const int k = reverse ? nc - 1 - i : i;
+        *nl += 2;
+        if ((rc = dg_residual_cells(L, x, b, r, L->pcol_cells[k].ptr, L->pcol_cells[k].count, st)))
+          return rc;
+        if ((rc = dg_patch_fdm(L, r, x, omega, L->pcol[k].ptr, L->pcol[k].count, 0, st)))
+          return rc;
+      }
+      return DG_OK;
+    }
+  }
+  return fail(DG_EINVAL, "unknown smoother kind");
+}
+
+int dg_smooth(dg_level_t* L, int kind, double omega, int reverse, double* x, const double* b,
+              double* r, int use_graph, void* stream) {
+  if (!L || !x || !b || !r) return fail(DG_EINVAL, "null argument");
+  if (r == x || r == b) return fail(DG_EINVAL, "scratch residual must not alias x or b");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!use_graph) return smooth_launches(L, kind, omega, reverse, x, b, r, st, &L->last_launches);
+  GraphKey key{kind, omega, reverse ? 1 : 0, x, b, r};
+  auto it = L->graphs.find(key);
+  if (it == L->graphs.end()) {
+    if (L->graphs.size() >= 32) {
+      cudaGraphExecDestroy(L->graphs.begin()->second);
+      L->graphs.erase(L->graphs.begin());
+    }
+    DG_CUDA(cudaStreamBeginCapture(L->cap, cudaStreamCaptureModeThreadLocal));
+    int64_t nl = 0;
+    int rc = smooth_launches(L, kind, omega, reverse, x, b, r, L->cap, &nl);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(L->cap, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(DG_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(DG_ECUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+    it = L->graphs.emplace(key, exec).first;
+    L->last_launches = nl;
+  }
+  DG_CUDA(cudaGraphLaunch(it->second, st));
+  return DG_OK;
+}
+
+int64_t dg_last_launch_count(const dg_level_t* L) { return L ? L->last_launches : -1; }
+
+}  // extern "C"

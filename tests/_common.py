@@ -1,0 +1,37 @@
+"""Shared helpers: golden fixtures, seeded inputs, tolerances."""
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden.npz")
+REF_SRC = "/root/reference/pkg/src"
+
+# north star: relative L2 <= 1e-12 in fp64
+RTOL = 1e-12
+
+_gold = None
+
+
+def golden():
+    global _gold
+    if _gold is None:
+        _gold = dict(np.load(GOLDEN))
+    return _gold
+
+
+def inputs(n, seed=0):
+    """b ~ U[-1,1](seed), x0 ~ U[-1,1](seed+1)."""
+    b = np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+    x0 = np.random.default_rng(seed + 1).uniform(-1.0, 1.0, n)
+    return x0, b
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def have_reference():
+    return os.path.isdir(REF_SRC)

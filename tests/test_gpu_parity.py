@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path through the public API (C ABI underneath)
+against the reference's golden vectors and the pinned CPU oracle.
+
+Tolerance (north star): relative L2 <= 1e-12 in fp64; index maps bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+from _common import golden, inputs, rel, RTOL
+
+import paper_1910_11239_b200 as dg
+from paper_1910_11239_b200 import fastdiag as fd
+from paper_1910_11239_b200 import mesh as M
+from oracle.sipg_oracle import OracleLevel
+
+pytestmark = pytest.mark.gpu
+G = golden()
+OPS = sorted({k.split("/")[0] for k in G if k.startswith("op_")})
+STEPS = sorted({k.split("/")[0] for k in G if k.startswith("sm_")})
+
+
+def _setup(d, nc, k, kind="acs", omega=1.0):
+    lvl = dg.build_hierarchy(d, nc, 0).levels[0]
+    basis = dg.Basis1D.make(k)
+    ctx = dg.make_context(lvl, basis, 1.0)
+    sm = dg.make_level_smoother(ctx, basis, dg.SmootherConfig(kind=kind, omega=omega))
+    return ctx, basis, sm
+
+
+# ---------------------------------------------------------------- operator --
+@pytest.mark.parametrize("name", OPS)
+def test_operator_and_residual_match_reference(name):
+    _, d, k, nc = name.split("_")
+    ctx, _, _ = _setup(int(d[0]), int(nc[1:]), int(k[1:]))
+    x0, b = inputs(ctx.ndofs)
+    v = dg.apply_operator(ctx, x0)
+    assert rel(v, G[name + "/Ax"]) <= RTOL
+    r = np.empty(ctx.ndofs)
+    out = dg.residual(ctx, x0, b, out=r)
+    assert out is r and rel(r, G[name + "/res"]) <= RTOL
+    # torch zero-copy path gives the same bits as the numpy path
+    xt = torch.from_numpy(x0).cuda()
+    vt = dg.apply_operator(ctx, xt)
+    assert isinstance(vt, torch.Tensor) and np.array_equal(vt.cpu().numpy(), v)
+
+
+@pytest.mark.parametrize("d,nc,k", [(2, 64, 3), (3, 32, 3), (3, 16, 15), (3, 12, 7),
+                                    (3, 16, 5), (2, 9, 9), (3, 5, 11)])
+def test_operator_matches_oracle_at_size(d, nc, k):
+    ctx, _, _ = _setup(d, nc, k)
+    x0, b = inputs(ctx.ndofs, 11)
+    lvl = OracleLevel((nc,) * d, k)
+    assert rel(dg.apply_operator(ctx, x0), lvl.apply(x0)) <= RTOL
+    r = np.empty(ctx.ndofs)
+    assert rel(dg.residual(ctx, x0, b, out=r), lvl.residual(x0, b)) <= RTOL
+
+
+def test_operator_symmetric_full_cfg5_size():
+    """Size-independent property at the cfg-5 size (64^3 Q5): u.Av = v.Au."""
+    ctx, _, _ = _setup(3, 64, 5)
+    u = torch.rand(ctx.ndofs, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(1)) - 0.5
+    v = torch.rand(ctx.ndofs, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(2)) - 0.5
+    au = dg.apply_operator(ctx, u)
+    av = dg.apply_operator(ctx, v)
+    a = float(torch.dot(u, av))
+    b = float(torch.dot(v, au))
+    assert abs(a - b) <= 1e-12 * float(torch.dot(u, au))
+    assert float(torch.dot(u, au)) > 0
+
+
+def test_operator_errors():
+    ctx, _, _ = _setup(2, 3, 2)
+    with pytest.raises(ValueError):
+        dg.apply_operator(ctx, np.zeros(ctx.ndofs + 1))
+    t = torch.zeros(ctx.ndofs, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        dg.apply_operator(ctx, t, out=t)
+    with pytest.raises(ValueError):
+        dg.residual(ctx, t, t.clone(), out=t)
+
+
+# --------------------------------------------------------------- smoothing --
+@pytest.mark.parametrize("name", STEPS)
+def test_smoothing_step_matches_reference(name):
+    kind = name.split("_")[1]
+    d, nc, k, om, rev = G[name + "/meta"]
+    ctx, _, sm = _setup(int(d), int(nc), int(k), kind, float(om))
+    x0, b = inputs(ctx.ndofs)
+    x = x0.copy()
+    sm.smooth(x, b, reverse=bool(rev))
+    assert rel(x, G[name + "/x"]) <= RTOL
+    assert rel(x - x0, G[name + "/x"] - x0) <= 1e-11
+
+
+@pytest.mark.parametrize("kind,d,nc,k,omega", [
+    ("acs", 2, 64, 3, 0.7),     # cfg 1 (full size)
+    ("avs", 3, 32, 3, 0.25),    # cfg 2 (full size)
+    ("acs", 3, 16, 15, 0.7),    # cfg 4 (full size)
+    ("mvs", 3, 10, 7, 1.0),     # cfg 3 at reduced n_c
+    ("avs", 3, 20, 5, 0.25),    # cfg 5 at reduced n_c
+    ("mcs", 3, 9, 4, 0.8),
+    ("mvs", 2, 17, 6, 1.0),
+])
+def test_smoothing_step_matches_oracle_at_size(kind, d, nc, k, omega):
+    ctx, _, sm = _setup(d, nc, k, kind, omega)
+    x0, b = inputs(ctx.ndofs, 3)
+    x = torch.from_numpy(x0).cuda()
+    sm.smooth(x, torch.from_numpy(b).cuda())
+    want = OracleLevel((nc,) * d, k).smooth(kind, omega, x0, b)
+    got = x.cpu().numpy()
+    assert rel(got, want) <= RTOL
+    assert rel(got - x0, want - x0) <= 1e-11
+
+
+def test_mvs_full_cfg3_last_colour_local_residuals_vanish():
+    """cfg 3 at full size (3D Q7, 32^3, 16 colours, omega=1): after the sweep,
+    R_j (b - A x) = 0 on every patch of the last colour (exact local solves)."""
+    ctx, _, sm = _setup(3, 32, 7, "mvs", 1.0)
+    x0, b = inputs(ctx.ndofs, 0)
+    x = torch.from_numpy(x0).cuda()
+    bd = torch.from_numpy(b).cuda()
+    sm.smooth(x, bd)
+    r = torch.empty_like(x)
+    dg.residual(ctx, x, bd, out=r)
+    last = sm.colors.sets[-1]
+    gi = torch.from_numpy(sm.set.gather_map(last)).cuda()
+    loc = r[gi]
+    assert float(loc.norm()) <= 1e-12 * float(bd.norm())
+    assert float(r.norm()) > 1e-3 * float(bd.norm())  # not trivially zero elsewhere
+
+
+def test_avs_full_cfg5_linear_in_b():
+    """cfg 5 at full size (64^3 Q5 AVS): S(x, 2b) - S(x, 0) = 2 (S(x, b) - S(x, 0))."""
+    ctx, _, sm = _setup(3, 64, 5, "avs", 0.25)
+    x0, b = inputs(ctx.ndofs, 0)
+    xd = torch.from_numpy(x0).cuda()
+    bd = torch.from_numpy(b).cuda()
+    outs = []
+    for s in (0.0, 1.0, 2.0):
+        x = xd.clone()
+        sm.smooth(x, bd * s)
+        outs.append(x)
+    d1 = outs[1] - outs[0]
+    d2 = outs[2] - outs[0]
+    assert float((d2 - 2 * d1).norm()) <= 1e-12 * float(d2.norm())
+
+
+def test_graph_and_direct_launch_agree_bitwise():
+    ctx, _, sm = _setup(3, 6, 3, "mvs", 1.0)
+    x0, b = inputs(ctx.ndofs)
+    x1 = x0.copy()
+    sm.use_graph = True
+    sm.smooth(x1, b)
+    x2 = x0.copy()
+    sm.use_graph = False
+    sm.smooth(x2, b)
+    assert np.array_equal(x1, x2)
+    x3 = x0.copy()
+    sm.use_graph = True
+    sm.smooth(x3, b)  # replay
+    assert np.array_equal(x1, x3)
+
+
+def test_colored_equals_uncolored_additive_patches():
+    """`test_smoothers.py:74-84` on the device: colour-by-colour writes vs one
+    atomic launch over all patches."""
+    ctx, _, sm = _setup(2, 8, 2, "avs", 0.2)
+    _, b = inputs(ctx.ndofs, 4)
+    x1 = np.zeros(ctx.ndofs)
+    sm.smooth_additive(x1, b)
+    x2 = np.zeros(ctx.ndofs)
+    sm.smooth_additive_uncolored(x2, b)
+    assert np.allclose(x1, x2, atol=1e-13 * max(1.0, np.abs(x1).max()))
+    x3 = np.zeros(ctx.ndofs)
+    rev = M.ColorPartition(sm.colors.n_subdomains, sm.colors.sets[::-1])
+    sm.smooth_additive(x3, b, colors=rev)
+    assert np.allclose(x1, x3, atol=1e-13 * max(1.0, np.abs(x1).max()))
+
+
+def test_exact_single_cell_and_single_patch_solves():
+    for d, nc, k, kind in ((2, 1, 3, "acs"), (2, 2, 2, "avs"), (3, 1, 4, "acs"), (3, 2, 2, "avs")):
+        ctx, _, sm = _setup(d, nc, k, kind, 1.0)
+        b = np.random.default_rng(0).standard_normal(ctx.ndofs)
+        x = np.zeros(ctx.ndofs)
+        sm.smooth(x, b)
+        r = b - dg.apply_operator(ctx, x)
+        assert np.linalg.norm(r) <= 1e-12 * np.linalg.norm(b)
+
+
+# ------------------------------------------------------------ solver sets --
+def test_solver_sets_match_reference():
+    lvl = dg.build_hierarchy(3, 4, 0).levels[0]
+    basis = dg.Basis1D.make(3)
+    ctx = dg.make_context(lvl, basis)
+    _, r = inputs(ctx.ndofs, 7)
+    cset = fd.CellSolverSet(lvl, basis, 1.0, ctx=ctx)
+    x = np.zeros(ctx.ndofs)
+    cset.solve_scaled_into(x, r, None, 1.0)
+    assert rel(x, G["cellset_3d_q3_n4/x"]) <= RTOL
+    x = np.zeros(ctx.ndofs)
+    cset.solve_scaled_into(x, r, np.array([0, 5, 21, 63]), 0.5)
+    assert rel(x, G["cellset_sub_3d_q3_n4/x"]) <= RTOL
+    touched = np.zeros(ctx.ndofs, bool)
+    for c in (0, 5, 21, 63):
+        touched[c * 64:(c + 1) * 64] = True
+    assert np.all(x[~touched] == 0.0)
+    pset = fd.PatchSolverSet(lvl, basis, 1.0, ctx=ctx)
+    x = np.zeros(ctx.ndofs)
+    pset.solve_scaled_into(x, r, None, 1.0, safe_accumulate=True)
+    assert rel(x, G["patchset_3d_q3_n4/x"]) <= RTOL
+    # reference per-class part format is accepted too
+    parts = [np.arange(len(rows)) for rows, _ in pset.classes]
+    x2 = np.zeros(ctx.ndofs)
+    pset.solve_partitioned(x2, r, parts, 1.0, safe_accumulate=True)
+    assert np.allclose(x2, x, rtol=0, atol=1e-13 * np.abs(x).max())
+
+
+# ------------------------------------------------------------- index maps --
+@pytest.mark.parametrize("name", ["map_3d_q3_n4", "map_2d_q2_n5", "map_3d_q1_n5"])
+def test_gather_maps_bit_exact(name):
+    _, d, k, nc = name.split("_")
+    lvl = dg.build_hierarchy(int(d[0]), int(nc[1:]), 0).levels[0]
+    basis = dg.Basis1D.make(int(k[1:]))
+    pset = fd.PatchSolverSet(lvl, basis, 1.0)
+    gi = pset.gather_map(np.arange(len(pset.patches)))
+    assert gi.dtype == np.int64 and np.array_equal(gi, G[name + "/gidx"])
+    assert np.array_equal(pset.subdomain_indices(3), G[name + "/gidx"][3])
+
+
+@pytest.mark.parametrize("name,d,nc", [("col_3d_n8", 3, 8), ("col_2d_n7", 2, 7),
+                                       ("col_3d_n5", 3, 5)])
+def test_device_colour_lists_bit_exact(name, d, nc):
+    ctx, _, sm = _setup(d, nc, 1, "mvs", 1.0)
+    dev = ctx.dev
+    ids = []
+    for c in range(dev.num_colours("mvs")):
+        ptr, cnt = dev.colour_list("mvs", c)
+        ids.append(_read_i32(ptr, cnt))
+    assert np.array_equal(np.concatenate(ids), G[name + "/patch_order"])
+    rb = [_read_i32(*dev.colour_list("mcs", c)) for c in range(dev.num_colours("mcs"))]
+    assert np.array_equal(np.concatenate(rb), G[name + "/rb_order"])
+
+
+def _read_i32(ptr, cnt):
+    """Copy a device int32 array owned by the level to the host."""
+    class _View:
+        __cuda_array_interface__ = {"shape": (cnt,), "typestr": "<i4",
+                                    "data": (ptr, True), "version": 3}
+    return torch.as_tensor(_View(), device="cuda").cpu().numpy().copy()
+
+
+def test_unsupported_patch_degree_raises():
+    lvl = dg.build_hierarchy(3, 3, 0).levels[0]
+    basis = dg.Basis1D.make(8)
+    ctx = dg.make_context(lvl, basis)
+    with pytest.raises(NotImplementedError):
+        dg.make_level_smoother(ctx, basis, dg.SmootherConfig("avs", 0.25))
