@@ -1,0 +1,392 @@
+"""Benchmark: fp64 Schwarz smoothing DoFs/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+
+Workload (default, BASELINE.json configs[4], the config quoted at 1/2/4/8
+GPUs): 3D Q5 SIPG Laplacian, additive vertex-patch Schwarz (12^3-DoF patches,
+16 structured colours, omega = 0.25) plus the matrix-free residual, fp64,
+64^3 cells per GPU; at N GPUs the box is 64 x 64 x 64N cells split in slabs
+along z with two ghost layers exchanged by NCCL (weak scaling).  A step is one
+additive smoothing step x <- x + omega sum_j R_j^T A_j^-1 R_j (b - A x).
+`--config 1..4` selects the other BASELINE configs (1 GPU only).
+
+Inputs: b, x0 ~ U[-1,1] from seeds 0/1 (synthetic); every vector
+(453 MB at cfg 5) is larger than the 126 MB L2, so no L2 flush is needed.
+
+`value` is device-timed (CUDA events, max over ranks) with inputs resident in
+HBM; `e2e` times the public API (`LevelSmoother.smooth`) with the host->device
+copy of x and b from pinned memory and the device->host copy of x inside the
+timed region.  `--impl reference` times the CPU oracle port of the reference
+algorithm (oracle/sipg_oracle.py; the reference itself is Python and cannot
+travel to the GPU box) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(d=2, nc=64, k=3, kind="acs", omega=0.7,
+            name="cfg1: 2D Q3 SIPG, 64^2 cells, additive cell Schwarz (ACS)"),
+    2: dict(d=3, nc=32, k=3, kind="avs", omega=0.25,
+            name="cfg2: 3D Q3 SIPG, 32^3 cells, additive vertex-patch Schwarz (AVS, 16 colours)"),
+    3: dict(d=3, nc=32, k=7, kind="mvs", omega=1.0,
+            name="cfg3: 3D Q7 SIPG, 32^3 cells, multiplicative vertex-patch sweep (MVS, 16 colours)"),
+    4: dict(d=3, nc=16, k=15, kind="acs", omega=0.7,
+            name="cfg4: 3D Q15 SIPG, 16^3 cells, additive cell Schwarz (ACS)"),
+    5: dict(d=3, nc=64, k=5, kind="avs", omega=0.25,
+            name="cfg5: 3D Q5 SIPG, 64^3 cells per GPU (64x64x64N slabs), AVS 12^3-DoF patches, 16 colours"),
+}
+METRIC = "fp64 Schwarz smoothing DoFs/s (1/2/4/8 B200) + % fp64/HBM roofline"
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def _fp64_peak():
+    """Measured fp64 peak (DMMA.8x8x4 loop, tools/microbench/fp64_peak.cu)."""
+    best = None
+    try:
+        with open(FP64_PEAK_FILE) as f:
+            for line in f:
+                rec = json.loads(line)
+                if "tflops" in rec:
+                    best = max(best or 0.0, rec["tflops"])
+    except (OSError, ValueError):
+        pass
+    return (best, "measured fp64 DMMA burst, profiles/r01_fp64_peak.json") if best else \
+        (37.0, "nominal fp64 (no measurement file)")
+
+
+def _hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, cfg):
+    """CPU oracle port of the reference path on a bounded sample (rank 0)."""
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    from oracle.sipg_oracle import OracleLevel, seeded_inputs
+    cores = len(os.sched_getaffinity(0))
+    d, nc, k = cfg["d"], cfg["nc"], cfg["k"]
+    # bounded sample: a slab of the same box (all of it for small configs)
+    if args.config == 5:
+        dims = (nc, nc, 4)
+        sample = f"64x64x4-cell slab of the 64^3 Q5 box ({nc * nc * 4 * 216} DoFs), one AVS step"
+    elif args.config == 3:
+        dims = (nc, nc, 4)
+        sample = "32x32x4-cell slab of the 32^3 Q7 box, one MVS sweep (16 colours)"
+    else:
+        dims = (nc,) * d
+        sample = "full level, one step"
+    lvl = OracleLevel(dims, k, h=1.0 / nc)
+    x0, b = seeded_inputs(lvl.ndofs, 0)
+    for _ in range(max(1, min(args.warmup, 1))):
+        lvl.smooth(cfg["kind"], cfg["omega"], x0, b)
+    t0 = time.perf_counter()
+    lvl.smooth(cfg["kind"], cfg["omega"], x0, b)
+    t_one = time.perf_counter() - t0
+    # bounded: at most ~150 s of timed CPU work whatever --steps says
+    n_run = max(1, min(args.steps, int(150.0 / max(t_one, 1e-3))))
+    times = []
+    for _ in range(n_run):
+        t0 = time.perf_counter()
+        lvl.smooth(cfg["kind"], cfg["omega"], x0, b)
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    value = lvl.ndofs / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DoF/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded uniform[-1,1])",
+        "config": {"workload": cfg["name"], "sample": sample, "k": k, "kind": cfg["kind"],
+                   "omega": cfg["omega"], "steps_run": n_run},
+        "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(cfg, config_id, budget_s=20.0):
+    """Oracle step on a bounded sample (rank 0, N=1), all host threads."""
+    from oracle.sipg_oracle import OracleLevel, seeded_inputs
+    d, nc, k = cfg["d"], cfg["nc"], cfg["k"]
+    if config_id == 5:
+        dims, sample = (nc, nc, 8), "one AVS step on a 64x64x8-cell slab of the Q5 box"
+    elif config_id == 3:
+        dims, sample = (nc, nc, 4), "one MVS sweep on a 32x32x4-cell slab of the Q7 box"
+    else:
+        dims, sample = (nc,) * d, "one step on the full level"
+    lvl = OracleLevel(dims, k, h=1.0 / nc)
+    x0, b = seeded_inputs(lvl.ndofs, 0)
+    times = []
+    t_all = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        lvl.smooth(cfg["kind"], cfg["omega"], x0, b)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget_s or len(times) >= 5:
+            break
+    t = float(min(times))
+    return {"value": lvl.ndofs / t, "unit": "DoF/s", "cores": len(os.sched_getaffinity(0)),
+            "kind": "port", "sample": f"{sample}, best of {len(times)}"}
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1910_11239_b200 as dg
+    from paper_1910_11239_b200 import flops as F
+
+    ws, rank, local = _dist_env()
+    if args.gpus != ws and ws > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    d, nc, k, kind, omega = cfg["d"], cfg["nc"], cfg["k"], cfg["kind"], cfg["omega"]
+    if ws > 1 and args.config != 5:
+        raise SystemExit("multi-GPU runs use the cfg-5 weak-scaling workload")
+    dims = (nc,) * d if ws == 1 else (nc, nc, nc * ws)
+
+    if ws == 1:
+        lvl = dg.build_hierarchy(d, nc, 0).levels[0]
+        basis = dg.Basis1D.make(k)
+        ctx = dg.make_context(lvl, basis, 1.0)
+        sm = dg.make_level_smoother(ctx, basis, dg.SmootherConfig(kind=kind, omega=omega))
+        n_local = ctx.ndofs
+        step_obj = sm
+    else:
+        from paper_1910_11239_b200.distributed import SlabSmoother
+        step_obj = SlabSmoother(dims, k, kind=kind, omega=omega, rank=rank, world=ws)
+        n_local = step_obj.n_owned
+    n_global = n_local * ws
+
+    # seeded inputs, generated on the host once (rank-local slab of the global vectors)
+    rng_off = rank * n_local
+    b_h = np.random.default_rng(0).uniform(-1.0, 1.0, n_global)[rng_off:rng_off + n_local] \
+        if ws > 1 else np.random.default_rng(0).uniform(-1.0, 1.0, n_local)
+    x_h = np.random.default_rng(1).uniform(-1.0, 1.0, n_global)[rng_off:rng_off + n_local] \
+        if ws > 1 else np.random.default_rng(1).uniform(-1.0, 1.0, n_local)
+    stream = torch.cuda.current_stream()
+
+    if ws == 1:
+        x = torch.from_numpy(x_h).cuda()
+        b = torch.from_numpy(b_h).cuda()
+
+        def step():
+            sm.smooth(x, b)
+    else:
+        step_obj.load(x_h, b_h)
+
+        def step():
+            step_obj.step()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = int(step_obj.launches_per_step())
+    clocks = ClockSampler(local)
+    time.sleep(0.2)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = n_global / (ms_step * 1e-3)
+
+    # ---- per-kernel split (dominant kernel for the roofline), direct launches
+    kt = step_obj.kernel_times(reps=max(3, min(args.steps, 10)))
+    flops_step, bytes_step = F.step_work(kind, d, k, dims if ws == 1 else (nc, nc, nc))
+    if kind in ("avs", "mvs"):
+        npatch = int(np.prod([v - 1 for v in (dims if ws == 1 else (nc, nc, nc))]))
+        f_solve = F.solve_flops(d, 2 * (k + 1), npatch)
+        dom = "fdm_kernel<3,12,patch> (all colours)" if k == 5 else "fdm_kernel<patch>"
+    else:
+        f_solve = F.solve_flops(d, k + 1, int(np.prod(dims)))
+        dom = "fdm_kernel<cell>"
+    f_res = flops_step - f_solve
+    peak, peak_src = _fp64_peak()
+    hbm, hbm_src = _hbm_peak()
+    solve_ms, res_ms = kt["solve_ms"], kt["residual_ms"]
+    dom_ms, dom_f = (solve_ms, f_solve) if solve_ms >= res_ms else (res_ms, f_res)
+    if solve_ms < res_ms:
+        dom = "residual_kernel"
+    achieved = dom_f / (dom_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(TRAFFIC_FILE) as f:
+            traffic = json.load(f).get(f"cfg{args.config}")
+    except (OSError, ValueError):
+        traffic = None
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if ws == 1:
+        xh = torch.from_numpy(x_h.copy()).pin_memory()
+        bh = torch.from_numpy(b_h.copy()).pin_memory()
+        xd = torch.empty_like(xh, device="cuda")
+        bd = torch.empty_like(bh, device="cuda")
+        for _ in range(2):
+            xd.copy_(xh, non_blocking=True)
+            bd.copy_(bh, non_blocking=True)
+            sm.smooth(xd, bd)
+            xh.copy_(xd, non_blocking=True)
+        torch.cuda.synchronize()
+        ke = max(3, min(args.steps, 20))
+        e0.record(stream)
+        for _ in range(ke):
+            xd.copy_(xh, non_blocking=True)
+            bd.copy_(bh, non_blocking=True)
+            sm.smooth(xd, bd)
+            xh.copy_(xd, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / ke
+        e2e = {"value": n_global / (e_ms * 1e-3), "unit": "DoF/s",
+               "h2d_bytes_per_step": 16 * n_local, "d2h_bytes_per_step": 8 * n_local,
+               "ms_per_step": e_ms, "api": "LevelSmoother.smooth(torch CUDA tensors), pinned H2D/D2H"}
+    else:
+        e2e = step_obj.e2e(x_h, b_h, reps=max(3, min(args.steps, 10)))
+        e2e["value"] = e2e.pop("dofs_local") * ws / (e2e["ms_per_step"] * 1e-3)
+        t = torch.tensor([e2e["ms_per_step"]], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e["ms_per_step"] = float(t.item())
+        e2e["value"] = n_global / (e2e["ms_per_step"] * 1e-3)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline_sample(cfg, args.config)
+
+    if rank == 0:
+        step_roof_ms = max(flops_step / (peak * 1e12), bytes_step / (hbm * 1e9)) * 1e3
+        line = {
+            "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded uniform[-1,1] b, x0)",
+            "config": {"workload": cfg["name"], "dims": list(dims), "k": k, "kind": kind,
+                       "omega": omega, "global_dofs": n_global,
+                       "parallelism": f"slab{ws}" if ws > 1 else "single",
+                       "l2": "inputs larger than L2 (no flush)" if n_local * 8 > 126e6
+                       else "inputs smaller than L2"},
+            "roofline": {"bound": "tensor", "pipe": "fp64 (DFMA/DMMA)", "kernel": dom,
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "step_frac": step_roof_ms / ms_step,
+                         "step_flops": flops_step, "step_bytes": bytes_step,
+                         "hbm_peak_gbs": hbm, "hbm_source": hbm_src,
+                         "kernel_ms": kt},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -246,7 +246,7 @@ def _read_i32(ptr, cnt):
     """Copy a device int32 array owned by the level to the host."""
     class _View:
         __cuda_array_interface__ = {"shape": (cnt,), "typestr": "<i4",
-                                    "data": (ptr, True), "version": 3}
+                                    "data": (ptr, False), "version": 3}
     return torch.as_tensor(_View(), device="cuda").cpu().numpy().copy()
 
 
