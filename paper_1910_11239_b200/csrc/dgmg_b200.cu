@@ -10,6 +10,8 @@
 //    131-166), captured once into CUDA graphs and replayed.
 #include "../../include/dgmg_b200.h"
 #include "kernels.cuh"
+#include "fdm2.cuh"
+#include "res2.cuh"
 
 #include <cuda_runtime.h>
 
@@ -65,35 +67,72 @@ __global__ void gather_map_kernel(MapParams p) {
 // ---------------------------------------------------------------------------
 // template dispatch
 // ---------------------------------------------------------------------------
+struct HostRes {
+  const double* mass;   // n*n
+  const double* adiag;  // 4*n*n
+  const double* bg;     // 2*n
+};
+
 template <int D, int N>
-static int launch_residual(const ResParams& p, cudaStream_t st) {
-  if (p.count <= 0) return DG_OK;
-  constexpr int G = groups_for(Lay<D, N>::F);
-  const size_t smem = sizeof(double) * res_smem_doubles<D, N>();
-  auto k = residual_kernel<D, N>;
+static int launch_residual(const ResParams& q, const HostRes& h, cudaStream_t st) {
+  if (q.count <= 0) return DG_OK;
+  constexpr int G = fdm2_groups<D, N>();
+  const size_t smem = sizeof(double) * res2_smem_doubles<D, N>();
+  auto k = res2_kernel<D, N>;
   static bool attr = false;
   if (!attr) {
     DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int64_t grid = (p.count + G - 1) / G;
+  Res2Params<D, N> p;
+  p.x = q.x;
+  p.b = q.b;
+  p.r = q.r;
+  p.list = q.list;
+  p.start = q.start;
+  p.count = q.count;
+  p.alpha = q.alpha;
+  p.beta = q.beta;
+  p.betap = q.betap;
+  p.geo = q.geo;
+  for (int i = 0; i < N; ++i)
+    for (int k = 0; k < N; ++k) {
+      p.mats.mass[k * N + i] = h.mass[i * N + k];
+      for (int dg = 0; dg < 4; ++dg) p.mats.adiag[dg][k * N + i] = h.adiag[dg * N * N + i * N + k];
+    }
+  std::memcpy(p.mats.bg0, h.bg, sizeof(p.mats.bg0));
+  std::memcpy(p.mats.bg1, h.bg + N, sizeof(p.mats.bg1));
+  const int64_t grid = (q.count + G - 1) / G;
   k<<<(unsigned)grid, G * Lay<D, N>::F, smem, st>>>(p);
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }
 
 template <int D, int M, bool PATCH>
-static int launch_fdm(const FdmParams& p, cudaStream_t st) {
-  if (p.count <= 0) return DG_OK;
-  constexpr int G = groups_for(Lay<D, M>::F);
-  const size_t smem = sizeof(double) * fdm_smem_doubles<D, M>();
-  auto k = fdm_kernel<D, M, PATCH>;
+static int launch_fdm(const FdmParams& q, const double* hz, const double* hzt, cudaStream_t st) {
+  if (q.count <= 0) return DG_OK;
+  constexpr int G = fdm2_groups<D, M>();
+  const size_t smem = sizeof(double) * fdm2_smem_doubles<D, M>();
+  auto k = fdm2_kernel<D, M, PATCH>;
   static bool attr = false;
   if (!attr) {
     DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int64_t grid = (p.count + G - 1) / G;
+  Fdm2Params<D, M> p;
+  p.r = q.r;
+  p.x = q.x;
+  p.list = q.list;
+  p.start = q.start;
+  p.count = q.count;
+  p.invsum = q.invsum;
+  p.omega = q.omega;
+  p.atomic = q.atomic;
+  p.geo = q.geo;
+  // fwd[k][i] = Z[k][i] (out = Z^T v); bwd[k][i] = Z^T[k][i] (out = Z v)
+  std::memcpy(p.mats.fwd, hz, sizeof(p.mats.fwd));
+  std::memcpy(p.mats.bwd, hzt, sizeof(p.mats.bwd));
+  const int64_t grid = (q.count + G - 1) / G;
   k<<<(unsigned)grid, G * Lay<D, M>::F, smem, st>>>(p);
   DG_CUDA(cudaGetLastError());
   return DG_OK;
@@ -103,8 +142,9 @@ static int launch_fdm(const FdmParams& p, cudaStream_t st) {
   X(D, 2) X(D, 3) X(D, 4) X(D, 5) X(D, 6) X(D, 7) X(D, 8) X(D, 9) X(D, 10) \
   X(D, 11) X(D, 12) X(D, 13) X(D, 14) X(D, 15) X(D, 16)
 
-static int dispatch_residual(int d, int n, const ResParams& p, cudaStream_t st) {
-#define X(D, N) if (d == D && n == N) return launch_residual<D, N>(p, st);
+static int dispatch_residual(int d, int n, const ResParams& p, const HostRes& h,
+                             cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_residual<D, N>(p, h, st);
   DG_N_CASES(X, 2)
   DG_N_CASES(X, 3)
 #undef X
@@ -112,8 +152,9 @@ static int dispatch_residual(int d, int n, const ResParams& p, cudaStream_t st) 
                                    ", n " + std::to_string(n));
 }
 
-static int dispatch_cell_fdm(int d, int n, const FdmParams& p, cudaStream_t st) {
-#define X(D, N) if (d == D && n == N) return launch_fdm<D, N, false>(p, st);
+static int dispatch_cell_fdm(int d, int n, const FdmParams& p, const double* hz,
+                             const double* hzt, cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_fdm<D, N, false>(p, hz, hzt, st);
   DG_N_CASES(X, 2)
   DG_N_CASES(X, 3)
 #undef X
@@ -121,8 +162,9 @@ static int dispatch_cell_fdm(int d, int n, const FdmParams& p, cudaStream_t st) 
                                    ", n " + std::to_string(n));
 }
 
-static int dispatch_patch_fdm(int d, int n, const FdmParams& p, cudaStream_t st) {
-#define X(D, N) if (d == D && n == N) return launch_fdm<D, 2 * N, true>(p, st);
+static int dispatch_patch_fdm(int d, int n, const FdmParams& p, const double* hz,
+                              const double* hzt, cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_fdm<D, 2 * N, true>(p, hz, hzt, st);
   X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
   X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 6) X(3, 7) X(3, 8)
 #undef X
@@ -164,6 +206,9 @@ struct dg_level {
   const double *pz = nullptr, *pzt = nullptr, *pinv = nullptr;
   double alpha = 0, beta = 0, betap = 0;
   bool has_patch = false;
+  std::vector<double> hcz, hczt, hpz, hpzt;  // host copies for the kernel parameter space
+  std::vector<double> hmass, hadiag, hbg;
+  HostRes hres() const { return HostRes{hmass.data(), hadiag.data(), hbg.data()}; }
   std::vector<DevList> rb;          // red-black owned cells (MCS)
   std::vector<DevList> pcol;        // patch colours (AVS / MVS)
   std::vector<DevList> pcol_cells;  // cells covered by a patch colour (MVS)
@@ -218,6 +263,14 @@ static FdmParams fdm_params(const dg_level* L, bool patch, const double* r, doub
   return p;
 }
 
+static int check_align(const dg_level* L, const void* a, const void* b, const void* c) {
+  if (L->n % 2) return DG_OK;  // odd n: scalar row access
+  for (const void* p : {a, b, c})
+    if (p && (reinterpret_cast<uintptr_t>(p) & 15))
+      return fail(DG_EINVAL, "vectors must be 16-byte aligned (even n uses 16-byte row access)");
+  return DG_OK;
+}
+
 static int check_layers(const dg_level* L, int z0, int z1) {
   const int lo = L->desc.z_begin, hi = L->desc.z_begin + L->desc.z_count;
   const int last = L->desc.ncells[L->d - 1];
@@ -248,6 +301,8 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   const int last = desc->ncells[d - 1];
   if (desc->z_begin < 0 || desc->z_count < 1 || desc->z_begin + desc->z_count > last)
     return fail(DG_EINVAL, "stored window outside the level");
+  if (!T->mass || !T->adiag || !T->bg || !T->cell_z || !T->cell_zt || !T->cell_invsum)
+    return fail(DG_EINVAL, "missing table");
   auto* L = new dg_level();
   L->desc = *desc;
   L->d = d;
@@ -266,6 +321,15 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   L->beta = T->beta;
   L->betap = T->betap;
   L->has_patch = T->patch_z != nullptr && n <= 8;
+  L->hmass.assign(T->mass, T->mass + n * n);
+  L->hadiag.assign(T->adiag, T->adiag + 4 * n * n);
+  L->hbg.assign(T->bg, T->bg + 2 * n);
+  L->hcz.assign(T->cell_z, T->cell_z + 4 * n * n);
+  L->hczt.assign(T->cell_zt, T->cell_zt + 4 * n * n);
+  if (L->has_patch) {
+    L->hpz.assign(T->patch_z, T->patch_z + 16 * n * n);
+    L->hpzt.assign(T->patch_zt, T->patch_zt + 16 * n * n);
+  }
   const int m = L->m;
   const int64_t pw = (d == 3) ? 64 : 16;  // 4^d classes
   const int64_t ce = L->cell_dofs, pe = (d == 3) ? (int64_t)m * m * m : (int64_t)m * m;
@@ -414,10 +478,11 @@ int dg_apply(const dg_level_t* L, const double* u, double* v, int z0, int z1, vo
   if (!L || !u || !v) return fail(DG_EINVAL, "null argument");
   if (u == v) return fail(DG_EINVAL, "apply_operator: output must not alias input");
   if (int rc = check_layers(L, z0, z1)) return rc;
+  if (int rc = check_align(L, u, v, nullptr)) return rc;
   ResParams p = res_params(L, u, nullptr, v);
   p.start = (int64_t)(z0 - L->desc.z_begin) * L->layer_cells;
   p.count = (int64_t)(z1 - z0) * L->layer_cells;
-  return dispatch_residual(L->d, L->n, p, (cudaStream_t)stream);
+  return dispatch_residual(L->d, L->n, p, L->hres(), (cudaStream_t)stream);
 }
 
 int dg_residual(const dg_level_t* L, const double* x, const double* b, double* r, int z0,
@@ -425,26 +490,29 @@ int dg_residual(const dg_level_t* L, const double* x, const double* b, double* r
   if (!L || !x || !b || !r) return fail(DG_EINVAL, "null argument");
   if (r == x) return fail(DG_EINVAL, "residual: output must not alias x");
   if (int rc = check_layers(L, z0, z1)) return rc;
+  if (int rc = check_align(L, x, b, r)) return rc;
   ResParams p = res_params(L, x, b, r);
   p.start = (int64_t)(z0 - L->desc.z_begin) * L->layer_cells;
   p.count = (int64_t)(z1 - z0) * L->layer_cells;
-  return dispatch_residual(L->d, L->n, p, (cudaStream_t)stream);
+  return dispatch_residual(L->d, L->n, p, L->hres(), (cudaStream_t)stream);
 }
 
 int dg_residual_cells(const dg_level_t* L, const double* x, const double* b, double* r,
                       const int32_t* cells, int64_t n_cells, void* stream) {
   if (!L || !x || !b || !r || (!cells && n_cells > 0)) return fail(DG_EINVAL, "null argument");
   if (r == x) return fail(DG_EINVAL, "residual: output must not alias x");
+  if (int rc = check_align(L, x, b, r)) return rc;
   ResParams p = res_params(L, x, b, r);
   p.list = cells;
   p.count = n_cells;
-  return dispatch_residual(L->d, L->n, p, (cudaStream_t)stream);
+  return dispatch_residual(L->d, L->n, p, L->hres(), (cudaStream_t)stream);
 }
 
 int dg_cell_fdm(const dg_level_t* L, const double* r, double* x, double omega,
                 const int32_t* cells, int64_t n_cells, void* stream) {
   if (!L || !r || !x) return fail(DG_EINVAL, "null argument");
   if (r == x) return fail(DG_EINVAL, "cell solve: r must not alias x");
+  if (int rc = check_align(L, r, x, nullptr)) return rc;
   FdmParams p = fdm_params(L, false, r, x, omega);
   if (cells) {
     p.list = cells;
@@ -453,20 +521,21 @@ int dg_cell_fdm(const dg_level_t* L, const double* r, double* x, double omega,
     p.start = (int64_t)(L->desc.own_begin - L->desc.z_begin) * L->layer_cells;
     p.count = (int64_t)(L->desc.own_end - L->desc.own_begin) * L->layer_cells;
   }
-  return dispatch_cell_fdm(L->d, L->n, p, (cudaStream_t)stream);
+  return dispatch_cell_fdm(L->d, L->n, p, L->hcz.data(), L->hczt.data(), (cudaStream_t)stream);
 }
 
 int dg_patch_fdm(const dg_level_t* L, const double* r, double* x, double omega,
                  const int32_t* patches, int64_t n_patches, int atomic, void* stream) {
   if (!L || !r || !x || (!patches && n_patches > 0)) return fail(DG_EINVAL, "null argument");
   if (r == x) return fail(DG_EINVAL, "patch solve: r must not alias x");
+  if (int rc = check_align(L, r, x, nullptr)) return rc;
   if (!L->has_patch)
     return fail(DG_EUNSUPPORTED, "vertex-patch tables not available (degree > 7?)");
   FdmParams p = fdm_params(L, true, r, x, omega);
   p.list = patches;
   p.count = n_patches;
   p.atomic = atomic;
-  return dispatch_patch_fdm(L->d, L->n, p, (cudaStream_t)stream);
+  return dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), (cudaStream_t)stream);
 }
 
 int dg_num_colours(const dg_level_t* L, int kind) {
@@ -519,7 +588,7 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
     p.start = (int64_t)(L->desc.res_begin - L->desc.z_begin) * L->layer_cells;
     p.count = (int64_t)(L->desc.res_end - L->desc.res_begin) * L->layer_cells;
     ++*nl;
-    return dispatch_residual(L->d, L->n, p, st);
+    return dispatch_residual(L->d, L->n, p, L->hres(), st);
   };
   switch (kind) {
     case DG_ACS: {

@@ -1,0 +1,265 @@
+// fdm2.cuh - fast-diagonalisation solves, v2 (constant-operand DFMA).
+//
+// x += omega * Z Lambda^-1 Z^T R r for cells or vertex patches
+// (fastdiag.py:457-496, 602-628).  Design:
+//  - the 1D eigenvector matrices Z, Z^T of the four boundary digits travel in
+//    the kernel's parameter space (__grid_constant__); the matvec runs k-outer
+//    over a transposed-stored matrix so each LDCU.128 feeds two DFMAs with
+//    their constant operand and the tensor is the only shared-memory traffic;
+//  - one tensor buffer per subdomain: each thread owns one fiber of the
+//    contracted direction, reads it to registers, writes the result back in
+//    place (fibers of one direction partition the tensor);
+//  - the last forward contraction, the 1/Lambda-sum scaling and the first
+//    backward contraction act on the same fiber and are fused (2d-1 passes);
+//  - gather / scatter move whole cell rows (n contiguous doubles of one
+//    cell, 16-byte vectors when n is even) so index math is per row, not per
+//    element; a patch row lands at (s0 n, s1 n + i1, s2 n + i2) of the patch
+//    tensor (fastdiag.py:546-557);
+//  - several subdomains per CTA so that the CTA is a whole number of warps.
+#pragma once
+#include "kernels.cuh"
+
+namespace dgb {
+
+template <int M>
+struct FdmMats {
+  double fwd[4][M * M];  // Z per digit, row-major: fwd[k][i] = Z[k][i] -> out = Z^T v
+  double bwd[4][M * M];  // Z^T per digit, row-major: bwd[k][i] = Z[i][k] -> out = Z v
+};
+
+template <int D, int M>
+__host__ __device__ constexpr int fdm2_groups() {
+  constexpr int F = Lay<D, M>::F;
+  for (int g = 1; g <= 32; ++g)
+    if ((g * F) % 32 == 0 && g * F >= 128 && g * F <= 512) return g;
+  return F >= 128 ? 1 : (128 + F - 1) / F;
+}
+
+template <int D, int M>
+struct Fdm2Params {
+  const double* r;
+  double* x;
+  const int32_t* list;
+  int64_t start;
+  int64_t count;
+  const double* invsum;
+  double omega;
+  int atomic;
+  Geo geo;
+  FdmMats<M> mats;
+};
+
+// out_i = sum_k St[k*M+i] v_k  (k outer: constants consumed in load order)
+template <int M>
+__device__ __forceinline__ void matvec_t(const double* __restrict__ St, const double (&v)[M],
+                                         double (&o)[M]) {
+#pragma unroll
+  for (int i = 0; i < M; ++i) o[i] = St[i] * v[0];
+#pragma unroll
+  for (int k = 1; k < M; ++k) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) o[i] = fma(St[k * M + i], v[k], o[i]);
+  }
+}
+
+// compile-time matrix addresses for each digit (warp-uniform in practice)
+template <int M>
+__device__ __forceinline__ void matvec_digit(const double (&S)[4][M * M], int digit,
+                                             const double (&v)[M], double (&o)[M]) {
+  switch (digit) {
+    case 0: matvec_t<M>(S[0], v, o); break;
+    case 1: matvec_t<M>(S[1], v, o); break;
+    case 2: matvec_t<M>(S[2], v, o); break;
+    default: matvec_t<M>(S[3], v, o); break;
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void fiber_inplace(const double (&S)[4][M * M], int digit, double* buf,
+                                              int base, int stride) {
+  double v[M], o[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) v[k] = buf[base + k * stride];
+  matvec_digit<M>(S, digit, v, o);
+#pragma unroll
+  for (int k = 0; k < M; ++k) buf[base + k * stride] = o[k];
+}
+
+// one row of N doubles: global <-> shared
+template <int N>
+__device__ __forceinline__ void row_load(double* __restrict__ s, const double* __restrict__ g) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(g + i));
+      s[i] = v.x;
+      s[i + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) s[i] = __ldg(g + i);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void row_update(double* __restrict__ g, const double* __restrict__ s,
+                                           double omega, bool atomic) {
+  if (atomic) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) atomicAdd(g + i, omega * s[i]);
+    return;
+  }
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      double2 v = *reinterpret_cast<const double2*>(g + i);
+      v.x = fma(omega, s[i], v.x);
+      v.y = fma(omega, s[i + 1], v.y);
+      *reinterpret_cast<double2*>(g + i) = v;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) g[i] = fma(omega, s[i], g[i]);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void row_load_reg(double (&v)[N], const double* __restrict__ g) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      const double2 t = __ldg(reinterpret_cast<const double2*>(g + i));
+      v[i] = t.x;
+      v[i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = __ldg(g + i);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void row_store(double* __restrict__ g, const double (&v)[N]) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) *reinterpret_cast<double2*>(g + i) = make_double2(v[i], v[i + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) g[i] = v[i];
+  }
+}
+
+// rows of a subdomain: (cell slot, i1, i2) -> (global offset, shared offset)
+template <int D, int M, bool PATCH>
+struct Rows {
+  static constexpr int N = PATCH ? M / 2 : M;
+  static constexpr int RPC = (D == 3) ? N * N : N;      // rows per cell
+  static constexpr int SLOTS = PATCH ? (1 << D) : 1;     // cells per subdomain
+  static constexpr int RPS = SLOTS * RPC;                // rows per subdomain
+  __device__ __forceinline__ static void map(int rr, int& slot, int& goff, int& soff) {
+    using L = Lay<D, M>;
+    slot = rr / RPC;
+    const int w = rr - slot * RPC;
+    goff = w * N;
+    const int i1 = (D == 3) ? w % N : w;
+    const int i2 = (D == 3) ? w / N : 0;
+    const int s0 = slot & 1, s1 = (slot >> 1) & 1, s2 = (slot >> 2) & 1;
+    soff = s0 * N + L::P * (s1 * N + i1) + (D == 3 ? L::P * M * (s2 * N + i2) : 0);
+  }
+};
+
+template <int D, int M, bool PATCH>
+__global__ void __launch_bounds__(fdm2_groups<D, M>() * Lay<D, M>::F)
+fdm2_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
+  using L = Lay<D, M>;
+  using R = Rows<D, M, PATCH>;
+  constexpr int N = R::N;
+  constexpr int NEc = (D == 3) ? N * N * N : N * N;
+  constexpr int G = fdm2_groups<D, M>();
+  constexpr int F = L::F;
+  constexpr int NT = G * F;
+  extern __shared__ double sm[];
+  __shared__ int s_info[G][8];            // digit[3], cls, active
+  __shared__ int64_t s_cell[G][R::SLOTS];  // dof offset of each cell of the subdomain
+  const int tid = threadIdx.x;
+  if (tid < G) {
+    const int64_t idx = (int64_t)blockIdx.x * G + tid;
+    int* inf = s_info[tid];
+    inf[7] = idx < p.count;
+    int digit[3] = {0, 0, 0}, base[3] = {0, 0, 0};
+    if (inf[7]) {
+      const int id = p.list ? p.list[idx] : (int)(p.start + idx);
+      subdomain_info<D, PATCH>(p.geo, id, digit, base);
+    }
+    int cls = 0;
+#pragma unroll
+    for (int t = D - 1; t >= 0; --t) cls = cls * 4 + digit[t];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) inf[t] = digit[t];
+    inf[6] = cls;
+#pragma unroll
+    for (int s = 0; s < R::SLOTS; ++s) {
+      int c[3] = {base[0] + (s & 1), base[1] + ((s >> 1) & 1), base[2] + ((s >> 2) & 1)};
+      if (!PATCH) c[0] = base[0], c[1] = base[1], c[2] = base[2];
+      s_cell[tid][s] = (int64_t)cell_local<D>(p.geo, c) * NEc;
+    }
+  }
+  __syncthreads();
+  // gather R_j r, one cell row per thread iteration
+  for (int row = tid; row < G * R::RPS; row += NT) {
+    const int g = row / R::RPS;
+    if (!s_info[g][7]) continue;
+    int slot, goff, soff;
+    R::map(row - g * R::RPS, slot, goff, soff);
+    row_load<N>(sm + g * L::SZ + soff, p.r + s_cell[g][slot] + goff);
+  }
+  __syncthreads();
+  const int g = tid / F, f = tid - (tid / F) * F;
+  const bool active = s_info[g][7];
+  const int* dg = s_info[g];
+  double* buf = sm + g * L::SZ;
+  // forward contractions with Z^T, directions 0 .. D-2
+#pragma unroll
+  for (int t = 0; t < D - 1; ++t) {
+    if (active) fiber_inplace<M>(p.mats.fwd, dg[t], buf, L::sbase(t, f), L::sstride(t));
+    __syncthreads();
+  }
+  // fused: Z^T along D-1, scale by 1/Lambda-sum, Z along D-1
+  if (active) {
+    constexpr int t = D - 1;
+    const int sb = L::sbase(t, f), ss = L::sstride(t);
+    const double* inv = p.invsum + (int64_t)dg[6] * L::NE + L::gbase(t, f);
+    double v[M], o[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) v[k] = buf[sb + k * ss];
+    matvec_digit<M>(p.mats.fwd, dg[t], v, o);
+#pragma unroll
+    for (int k = 0; k < M; ++k) o[k] *= __ldg(inv + k * L::gstride(t));
+    matvec_digit<M>(p.mats.bwd, dg[t], o, v);
+#pragma unroll
+    for (int k = 0; k < M; ++k) buf[sb + k * ss] = v[k];
+  }
+  __syncthreads();
+  // backward contractions with Z, directions D-2 .. 0
+#pragma unroll
+  for (int s = 0; s < D - 1; ++s) {
+    const int t = D - 2 - s;
+    if (active) fiber_inplace<M>(p.mats.bwd, dg[t], buf, L::sbase(t, f), L::sstride(t));
+    __syncthreads();
+  }
+  // scatter-add omega * R_j^T y, one cell row per thread iteration
+  for (int row = tid; row < G * R::RPS; row += NT) {
+    const int gg = row / R::RPS;
+    if (!s_info[gg][7]) continue;
+    int slot, goff, soff;
+    R::map(row - gg * R::RPS, slot, goff, soff);
+    row_update<N>(p.x + s_cell[gg][slot] + goff, sm + gg * L::SZ + soff, p.omega, p.atomic != 0);
+  }
+}
+
+template <int D, int M>
+__host__ __device__ constexpr int fdm2_smem_doubles() {
+  return fdm2_groups<D, M>() * Lay<D, M>::SZ;
+}
+
+}  // namespace dgb

@@ -1,0 +1,206 @@
+// res2.cuh - SIPG residual r = b - A x, v2 (constant-operand DFMA).
+//
+// dgop.residual / apply_operator (dgop.py:762-788) on a uniform Cartesian
+// level in Kronecker-sum form:
+//   A x |_c = sum_t (x)_{s != t} M_s  G_t,
+//   G_t = A_diag(digit_t) ._t x_c + a_pm ._t x_{c+e_t} + a_pm^T ._t x_{c-e_t},
+// with a_pm = alpha e_{n-1} e_0^T + beta e_{n-1} bg0^T + beta' bg1 e_0^T
+// (polybasis.py:278-284; bv0 = e_0, bv1 = e_{n-1} on GL nodes).
+//
+// The 1D matrices (M, A_diag per digit) and the basis derivatives live in the
+// kernel parameter space, so the DFMAs take their matrix operand from the
+// constant bank.  Per cell three shared buffers X, A, B and five phases
+// (3D; 8 contractions):
+//   1: A = G_0(X) [fibers t=0],  B = G_1(X) [t=1]
+//   2: A <- M A   [t=1],         B <- M B   [t=0]
+//   3: A <- M (A + B) [t=2],     B = G_2(X) [t=2]     (same fiber: no race)
+//   4: B <- M B   [t=1]
+//   5: A <- A + M B [t=0]; then r = b - A (coalesced)
+#pragma once
+#include "kernels.cuh"
+#include "fdm2.cuh"
+
+namespace dgb {
+
+template <int N>
+struct ResMats {
+  double mass[N * N];      // stored transposed (matvec_t): mass[k][i] = M[i][k]
+  double adiag[4][N * N];  // transposed A_diag per digit
+  double bg0[N];
+  double bg1[N];
+};
+
+template <int D, int N>
+struct Res2Params {
+  const double* x;
+  const double* b;  // nullptr: v = A x
+  double* r;
+  const int32_t* list;
+  int64_t start;
+  int64_t count;
+  double alpha, beta, betap;
+  Geo geo;
+  ResMats<N> mats;
+};
+
+// G_t fiber: A_diag(digit) along t plus the rank-2 neighbour couplings
+template <int D, int N>
+__device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, int f,
+                                             const int* c, const double* X, double* out) {
+  using L = Lay<D, N>;
+  const int sb = L::sbase(t, f), ss = L::sstride(t);
+  const int digit = (c[t] == 0 ? 1 : 0) | (c[t] == p.geo.nc[t] - 1 ? 2 : 0);
+  // neighbour fibers first (global loads in flight during the matvec)
+  const int gb = L::gbase(t, f), gs = L::gstride(t);
+  double xr[N], xl[N];
+  int nb[3] = {c[0], c[1], D == 3 ? c[2] : 0};
+  if (!(digit & 2)) {
+    nb[t] = c[t] + 1;
+    const double* q = p.x + (int64_t)cell_local<D>(p.geo, nb) * L::NE + gb;
+#pragma unroll
+    for (int k = 0; k < N; ++k) xr[k] = __ldg(q + k * gs);
+  }
+  if (!(digit & 1)) {
+    nb[t] = c[t] - 1;
+    const double* q = p.x + (int64_t)cell_local<D>(p.geo, nb) * L::NE + gb;
+#pragma unroll
+    for (int k = 0; k < N; ++k) xl[k] = __ldg(q + k * gs);
+  }
+  double v[N], o[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = X[sb + k * ss];
+  matvec_digit<N>(p.mats.adiag, digit, v, o);
+  if (!(digit & 2)) {  // a_pm x_R: value and normal derivative at the shared face
+    double g = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) g = fma(p.mats.bg0[k], xr[k], g);
+    const double fall = p.betap * xr[0];
+#pragma unroll
+    for (int i = 0; i < N; ++i) o[i] = fma(p.mats.bg1[i], fall, o[i]);
+    o[N - 1] += p.alpha * xr[0] + p.beta * g;
+  }
+  if (!(digit & 1)) {  // a_pm^T x_L
+    double g = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) g = fma(p.mats.bg1[k], xl[k], g);
+    const double fall = p.beta * xl[N - 1];
+#pragma unroll
+    for (int i = 0; i < N; ++i) o[i] = fma(p.mats.bg0[i], fall, o[i]);
+    o[0] += p.alpha * xl[N - 1] + p.betap * g;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) out[sb + i * ss] = o[i];
+}
+
+// buf <- M buf along t (in place), optionally adding `add` first
+template <int D, int N, bool ADD>
+__device__ __forceinline__ void mass_fiber(const Res2Params<D, N>& p, int t, int f, double* buf,
+                                           const double* add) {
+  using L = Lay<D, N>;
+  const int sb = L::sbase(t, f), ss = L::sstride(t);
+  double v[N], o[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = ADD ? buf[sb + k * ss] + add[sb + k * ss] : buf[sb + k * ss];
+  matvec_t<N>(p.mats.mass, v, o);
+#pragma unroll
+  for (int k = 0; k < N; ++k) buf[sb + k * ss] = o[k];
+}
+
+template <int D, int N>
+__global__ void __launch_bounds__(fdm2_groups<D, N>() * Lay<D, N>::F)
+res2_kernel(const __grid_constant__ Res2Params<D, N> p) {
+  using L = Lay<D, N>;
+  constexpr int G = fdm2_groups<D, N>();
+  constexpr int F = L::F;
+  constexpr int NT = G * F;
+  extern __shared__ double sm[];
+  __shared__ int s_cell[G];
+  const int tid = threadIdx.x;
+  if (tid < G) {
+    const int64_t idx = (int64_t)blockIdx.x * G + tid;
+    s_cell[tid] = idx < p.count ? (p.list ? p.list[idx] : (int)(p.start + idx)) : -1;
+  }
+  __syncthreads();
+  using R = Rows<D, N, false>;
+  for (int row = tid; row < G * R::RPS; row += NT) {
+    const int gg = row / R::RPS;
+    const int cell = s_cell[gg];
+    if (cell < 0) continue;
+    int slot, goff, soff;
+    R::map(row - gg * R::RPS, slot, goff, soff);
+    row_load<N>(sm + gg * L::SZ + soff, p.x + (int64_t)cell * L::NE + goff);
+  }
+  const int g = tid / F, f = tid - (tid / F) * F;
+  const int cell = s_cell[g];
+  const bool active = cell >= 0;
+  int c[3] = {0, 0, 0};
+  cell_multi<D>(p.geo, active ? cell : 0, c);
+  double* X = sm + g * L::SZ;
+  double* A = sm + (G + g) * L::SZ;
+  double* B = sm + (2 * G + g) * L::SZ;
+  __syncthreads();
+  if (active) {
+    stiff2_fiber<D, N>(p, 0, f, c, X, A);
+    stiff2_fiber<D, N>(p, 1, f, c, X, B);
+  }
+  __syncthreads();
+  if (active) {
+    mass_fiber<D, N, false>(p, 1, f, A, nullptr);
+    mass_fiber<D, N, false>(p, 0, f, B, nullptr);
+  }
+  __syncthreads();
+  if (D == 3) {
+    if (active) {
+      mass_fiber<D, N, true>(p, 2, f, A, B);   // A = M_2 (M_1 G_0 + M_0 G_1)
+      stiff2_fiber<D, N>(p, 2, f, c, X, B);    // B = G_2 (same fibers as above)
+    }
+    __syncthreads();
+    if (active) mass_fiber<D, N, false>(p, 1, f, B, nullptr);
+    __syncthreads();
+    if (active) {  // A += M_0 B
+      const int sb = L::sbase(0, f);
+      double v[N], o[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) v[k] = B[sb + k];
+      matvec_t<N>(p.mats.mass, v, o);
+#pragma unroll
+      for (int k = 0; k < N; ++k) A[sb + k] += o[k];
+    }
+  } else {
+    // 2D: OUT = M_1 G_0 + M_0 G_1 = A + B
+    if (active) {
+      const int sb = L::sbase(0, f);
+#pragma unroll
+      for (int k = 0; k < N; ++k) A[sb + k] += B[sb + k];
+    }
+  }
+  __syncthreads();
+  for (int row = tid; row < G * R::RPS; row += NT) {
+    const int gg = row / R::RPS;
+    const int cl = s_cell[gg];
+    if (cl < 0) continue;
+    int slot, goff, soff;
+    R::map(row - gg * R::RPS, slot, goff, soff);
+    const int64_t gi = (int64_t)cl * L::NE + goff;
+    const double* a = sm + (G + gg) * L::SZ + soff;
+    if (p.b) {
+      double bv[N];
+      row_load_reg<N>(bv, p.b + gi);
+#pragma unroll
+      for (int i = 0; i < N; ++i) bv[i] -= a[i];
+      row_store<N>(p.r + gi, bv);
+    } else {
+      double av[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) av[i] = a[i];
+      row_store<N>(p.r + gi, av);
+    }
+  }
+}
+
+template <int D, int N>
+__host__ __device__ constexpr int res2_smem_doubles() {
+  return 3 * fdm2_groups<D, N>() * Lay<D, N>::SZ;
+}
+
+}  // namespace dgb
