@@ -136,6 +136,11 @@ int dg_smooth(dg_level_t* lvl, int kind, double omega, int reverse,
 /* kernels launched by the last dg_smooth call (for the bench's count)      */
 int64_t dg_last_launch_count(const dg_level_t* lvl);
 
+/* 1 if the additive patch step (DG_AVS) of this level runs as the single
+ * persistent dataflow kernel (residual + all colours, L2-resident z-blocks),
+ * 0 if it runs as one residual launch plus one launch per colour.           */
+int dg_flow_enabled(const dg_level_t* lvl);
+
 #ifdef __cplusplus
 }
 #endif

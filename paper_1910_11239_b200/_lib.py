@@ -25,7 +25,7 @@ EXPORTS = (
     "dg_last_error", "dg_version", "dg_level_create", "dg_level_destroy",
     "dg_level_ndofs", "dg_apply", "dg_residual", "dg_residual_cells",
     "dg_cell_fdm", "dg_patch_fdm", "dg_num_colours", "dg_colour_list",
-    "dg_patch_gather_map", "dg_smooth", "dg_last_launch_count",
+    "dg_patch_gather_map", "dg_smooth", "dg_last_launch_count", "dg_flow_enabled",
 )
 
 
@@ -83,6 +83,7 @@ def load() -> ctypes.CDLL:
         "dg_patch_gather_map": ([vp, vp, i64, vp, vp], c_int),
         "dg_smooth": ([vp, c_int, c_double, c_int, vp, vp, vp, c_int, vp], c_int),
         "dg_last_launch_count": ([vp], i64),
+        "dg_flow_enabled": ([vp], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -9,9 +9,12 @@
 //  - the smoothing-step launch sequences of LevelSmoother (smoothers.py:
 //    131-166), captured once into CUDA graphs and replayed.
 #include "../../include/dgmg_b200.h"
-#include "kernels.cuh"
+#include "common.cuh"
 #include "fdm2.cuh"
 #include "res2.cuh"
+#include "flow.cuh"
+
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 
@@ -67,6 +70,42 @@ __global__ void gather_map_kernel(MapParams p) {
 // ---------------------------------------------------------------------------
 // template dispatch
 // ---------------------------------------------------------------------------
+// host-side launch arguments (the kernels' parameter structs are built from these)
+struct ResArgs {
+  const double* x = nullptr;
+  const double* b = nullptr;
+  double* r = nullptr;
+  const int32_t* list = nullptr;
+  int64_t start = 0;
+  int64_t count = 0;
+  int packed = 0;
+  double alpha = 0, beta = 0, betap = 0;
+  Geo geo;
+};
+
+struct FdmArgs {
+  const double* r = nullptr;
+  double* x = nullptr;
+  const int32_t* list = nullptr;
+  int64_t start = 0;
+  int64_t count = 0;
+  int packed = 0;
+  int atomic = 0;
+  const double* invsum = nullptr;
+  double omega = 0;
+  Geo geo;
+};
+
+template <typename K>
+static int resident_ctas(K k, int threads, size_t smem, int* out) {
+  int per_sm = 0, dev = 0, sms = 0;
+  DG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem));
+  DG_CUDA(cudaGetDevice(&dev));
+  DG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  *out = std::max(1, per_sm) * sms;
+  return DG_OK;
+}
+
 struct HostRes {
   const double* mass;   // n*n
   const double* adiag;  // 4*n*n
@@ -74,16 +113,10 @@ struct HostRes {
 };
 
 template <int D, int N>
-static int launch_residual(const ResParams& q, const HostRes& h, cudaStream_t st) {
+static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) {
   if (q.count <= 0) return DG_OK;
   constexpr int G = fdm2_groups<D, N>();
-  const size_t smem = sizeof(double) * res2_smem_doubles<D, N>();
-  auto k = res2_kernel<D, N>;
-  static bool attr = false;
-  if (!attr) {
-    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  constexpr int NT = G * Lay<D, N>::F;
   Res2Params<D, N> p;
   p.x = q.x;
   p.b = q.b;
@@ -91,6 +124,7 @@ static int launch_residual(const ResParams& q, const HostRes& h, cudaStream_t st
   p.list = q.list;
   p.start = q.start;
   p.count = q.count;
+  p.packed = q.packed;
   p.alpha = q.alpha;
   p.beta = q.beta;
   p.betap = q.betap;
@@ -102,14 +136,21 @@ static int launch_residual(const ResParams& q, const HostRes& h, cudaStream_t st
     }
   std::memcpy(p.mats.bg0, h.bg, sizeof(p.mats.bg0));
   std::memcpy(p.mats.bg1, h.bg + N, sizeof(p.mats.bg1));
-  const int64_t grid = (q.count + G - 1) / G;
-  k<<<(unsigned)grid, G * Lay<D, N>::F, smem, st>>>(p);
+  const int64_t ngroups = (q.count + G - 1) / G;
+  const size_t smem = sizeof(double) * res2_smem_doubles<D, N>();
+  auto k = res2_kernel<D, N>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k<<<(unsigned)ngroups, NT, smem, st>>>(p);
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }
 
 template <int D, int M, bool PATCH>
-static int launch_fdm(const FdmParams& q, const double* hz, const double* hzt, cudaStream_t st) {
+static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, cudaStream_t st) {
   if (q.count <= 0) return DG_OK;
   constexpr int G = fdm2_groups<D, M>();
   const size_t smem = sizeof(double) * fdm2_smem_doubles<D, M>();
@@ -128,6 +169,7 @@ static int launch_fdm(const FdmParams& q, const double* hz, const double* hzt, c
   p.invsum = q.invsum;
   p.omega = q.omega;
   p.atomic = q.atomic;
+  p.packed = q.packed;
   p.geo = q.geo;
   // fwd[k][i] = Z[k][i] (out = Z^T v); bwd[k][i] = Z^T[k][i] (out = Z v)
   std::memcpy(p.mats.fwd, hz, sizeof(p.mats.fwd));
@@ -138,11 +180,94 @@ static int launch_fdm(const FdmParams& q, const double* hz, const double* hzt, c
   return DG_OK;
 }
 
+struct FlowDev {
+  FlowTask* tasks = nullptr;
+  int32_t* item_task = nullptr;
+  int32_t* plist = nullptr;
+  unsigned* ctrl = nullptr;
+  int ntasks = 0;
+  int64_t nitems = 0;
+};
+
+template <int D, int N>
+static int launch_flow(const ResArgs& ra, const FdmArgs& fa, const HostRes& h, const double* hz,
+                       const double* hzt, const FlowDev& fd, cudaStream_t st) {
+  using S = FlowShape<D, N>;
+  constexpr int M = 2 * N;
+  const size_t smem = sizeof(double) * S::SMEM;
+  auto k = flow_kernel<D, N>;
+  static int resident = 0;
+  if (!resident) {
+    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (int rc = resident_ctas(k, S::NT, smem, &resident)) return rc;
+  }
+  FlowParams<D, N> p;
+  Res2Params<D, N>& r = p.res;
+  r.x = ra.x;
+  r.b = ra.b;
+  r.r = ra.r;
+  r.list = nullptr;
+  r.start = 0;
+  r.count = 0;
+  r.packed = 0;
+  r.alpha = ra.alpha;
+  r.beta = ra.beta;
+  r.betap = ra.betap;
+  r.geo = ra.geo;
+  for (int i = 0; i < N; ++i)
+    for (int kk = 0; kk < N; ++kk) {
+      r.mats.mass[kk * N + i] = h.mass[i * N + kk];
+      for (int dg = 0; dg < 4; ++dg) r.mats.adiag[dg][kk * N + i] = h.adiag[dg * N * N + i * N + kk];
+    }
+  std::memcpy(r.mats.bg0, h.bg, sizeof(r.mats.bg0));
+  std::memcpy(r.mats.bg1, h.bg + N, sizeof(r.mats.bg1));
+  Fdm2Params<D, M>& f = p.fdm;
+  f.r = fa.r;
+  f.x = fa.x;
+  f.list = nullptr;
+  f.start = 0;
+  f.count = 0;
+  f.invsum = fa.invsum;
+  f.omega = fa.omega;
+  f.atomic = 0;
+  f.packed = 1;
+  f.geo = fa.geo;
+  std::memcpy(f.mats.fwd, hz, sizeof(f.mats.fwd));
+  std::memcpy(f.mats.bwd, hzt, sizeof(f.mats.bwd));
+  p.tasks = fd.tasks;
+  p.item_task = fd.item_task;
+  p.plist = fd.plist;
+  p.nitems = fd.nitems;
+  p.ctrl = fd.ctrl;
+  DG_CUDA(cudaMemsetAsync(fd.ctrl, 0, sizeof(unsigned) * (1 + fd.ntasks), st));
+  k<<<(unsigned)std::min<int64_t>(fd.nitems, resident), S::NT, smem, st>>>(p);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
+static bool flow_shape(int d, int n, int* gp, int* gr) {
+#define X(D, N) \
+  if (d == D && n == N) { *gp = FlowShape<D, N>::GP; *gr = FlowShape<D, N>::GR; return true; }
+  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
+  X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 6) X(3, 7) X(3, 8)
+#undef X
+  return false;
+}
+
+static int dispatch_flow(int d, int n, const ResArgs& ra, const FdmArgs& fa, const HostRes& h,
+                         const double* hz, const double* hzt, const FlowDev& fd, cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_flow<D, N>(ra, fa, h, hz, hzt, fd, st);
+  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
+  X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 6) X(3, 7) X(3, 8)
+#undef X
+  return fail(DG_EUNSUPPORTED, "flow: no kernel");
+}
+
 #define DG_N_CASES(X, D) \
   X(D, 2) X(D, 3) X(D, 4) X(D, 5) X(D, 6) X(D, 7) X(D, 8) X(D, 9) X(D, 10) \
   X(D, 11) X(D, 12) X(D, 13) X(D, 14) X(D, 15) X(D, 16)
 
-static int dispatch_residual(int d, int n, const ResParams& p, const HostRes& h,
+static int dispatch_residual(int d, int n, const ResArgs& p, const HostRes& h,
                              cudaStream_t st) {
 #define X(D, N) if (d == D && n == N) return launch_residual<D, N>(p, h, st);
   DG_N_CASES(X, 2)
@@ -152,7 +277,7 @@ static int dispatch_residual(int d, int n, const ResParams& p, const HostRes& h,
                                    ", n " + std::to_string(n));
 }
 
-static int dispatch_cell_fdm(int d, int n, const FdmParams& p, const double* hz,
+static int dispatch_cell_fdm(int d, int n, const FdmArgs& p, const double* hz,
                              const double* hzt, cudaStream_t st) {
 #define X(D, N) if (d == D && n == N) return launch_fdm<D, N, false>(p, hz, hzt, st);
   DG_N_CASES(X, 2)
@@ -162,7 +287,7 @@ static int dispatch_cell_fdm(int d, int n, const FdmParams& p, const double* hz,
                                    ", n " + std::to_string(n));
 }
 
-static int dispatch_patch_fdm(int d, int n, const FdmParams& p, const double* hz,
+static int dispatch_patch_fdm(int d, int n, const FdmArgs& p, const double* hz,
                               const double* hzt, cudaStream_t st) {
 #define X(D, N) if (d == D && n == N) return launch_fdm<D, 2 * N, true>(p, hz, hzt, st);
   X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
@@ -209,9 +334,14 @@ struct dg_level {
   std::vector<double> hcz, hczt, hpz, hpzt;  // host copies for the kernel parameter space
   std::vector<double> hmass, hadiag, hbg;
   HostRes hres() const { return HostRes{hmass.data(), hadiag.data(), hbg.data()}; }
-  std::vector<DevList> rb;          // red-black owned cells (MCS)
-  std::vector<DevList> pcol;        // patch colours (AVS / MVS)
-  std::vector<DevList> pcol_cells;  // cells covered by a patch colour (MVS)
+  std::vector<DevList> rb;          // red-black owned cells (MCS), local ids
+  std::vector<DevList> rb_pk;       // same, packed global coordinates
+  std::vector<DevList> pcol;        // patch colours (AVS / MVS), global patch ids
+  std::vector<DevList> pcol_pk;     // same, packed vertex coordinates
+  std::vector<DevList> pcol_cells;  // cells covered by a patch colour (MVS), local ids
+  std::vector<DevList> pcol_cells_pk;
+  FlowDev flow;                     // dataflow AVS step (flow.cuh)
+  bool flow_ok = false;
   cudaStream_t cap = nullptr;       // capture stream
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int64_t last_launches = 0;
@@ -228,21 +358,22 @@ static int upload_list(const std::vector<int32_t>& h, DevList* out) {
 static void free_level(dg_level* L) {
   if (!L) return;
   for (auto& kv : L->graphs) cudaGraphExecDestroy(kv.second);
-  for (auto* v : {&L->rb, &L->pcol, &L->pcol_cells})
+  for (auto* v : {&L->rb, &L->rb_pk, &L->pcol, &L->pcol_pk, &L->pcol_cells, &L->pcol_cells_pk})
     for (auto& l : *v) cudaFree(l.ptr);
   cudaFree(L->dtab);
+  cudaFree(L->flow.tasks);
+  cudaFree(L->flow.item_task);
+  cudaFree(L->flow.plist);
+  cudaFree(L->flow.ctrl);
   if (L->cap) cudaStreamDestroy(L->cap);
   delete L;
 }
 
-static ResParams res_params(const dg_level* L, const double* x, const double* b, double* r) {
-  ResParams p{};
+static ResArgs res_params(const dg_level* L, const double* x, const double* b, double* r) {
+  ResArgs p;
   p.x = x;
   p.b = b;
   p.r = r;
-  p.mass = L->mass;
-  p.adiag = L->adiag;
-  p.bg = L->bg;
   p.alpha = L->alpha;
   p.beta = L->beta;
   p.betap = L->betap;
@@ -250,13 +381,11 @@ static ResParams res_params(const dg_level* L, const double* x, const double* b,
   return p;
 }
 
-static FdmParams fdm_params(const dg_level* L, bool patch, const double* r, double* x,
-                            double omega) {
-  FdmParams p{};
+static FdmArgs fdm_params(const dg_level* L, bool patch, const double* r, double* x,
+                          double omega) {
+  FdmArgs p;
   p.r = r;
   p.x = x;
-  p.z = patch ? L->pz : L->cz;
-  p.zt = patch ? L->pzt : L->czt;
   p.invsum = patch ? L->pinv : L->cinv;
   p.omega = omega;
   p.geo = L->geo;
@@ -279,6 +408,138 @@ static int check_layers(const dg_level* L, int z0, int z1) {
   // neighbours of computed layers must be stored (or be the physical boundary)
   if ((z0 > 0 && z0 - 1 < lo && z0 < z1) || (z1 < last && z1 >= hi && z0 < z1))
     return fail(DG_EINVAL, "residual layers need a stored neighbour layer on each side");
+  return DG_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// dataflow task graph of the AVS step (flow.cuh): z-blocks of `W` vertex
+// layers, colour skew `skew` between consecutive blocks.
+// ---------------------------------------------------------------------------
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+
+static int build_flow(dg_level* L) {
+  int gp = 0, gr = 0;
+  if (!L->has_patch || !flow_shape(L->d, L->n, &gp, &gr)) return DG_OK;
+  const int d = L->d;
+  const int* nc = L->desc.ncells;
+  for (int t = 0; t < d; ++t)
+    if (nc[t] < 2) return DG_OK;
+  const int W = std::max(1, env_int("DGB_FLOW_W", 2));
+  const int skew = std::max(0, env_int("DGB_FLOW_SKEW", 4));
+  const int zb = L->desc.z_begin;
+  const int vlo = std::max(1, L->desc.pv_begin), vhi = std::min(nc[d - 1] - 1, L->desc.pv_end);
+  struct HT {
+    int type, colour, blk, lo, hi;
+    int64_t start, count;
+    double key;
+    std::vector<int> deps;
+  };
+  std::vector<HT> ptasks;
+  std::vector<int32_t> plist;
+  const int ncol = 1 << (d + 1);
+  int64_t layer_patches = 1;
+  for (int t = 0; t < d - 1; ++t) layer_patches *= (nc[t] - 1);
+  // blocks aligned to global vertex layers 1 + W*k so that every window (slab)
+  // orders the colour updates of a DoF exactly as the single-GPU step does
+  for (int k0 = (vlo - 1) / W, blk = 0; 1 + k0 * W <= vhi; ++k0, ++blk) {
+    const int v0 = std::max(vlo, 1 + k0 * W);
+    const int v1 = std::min(vhi, k0 * W + W);
+    std::vector<std::vector<int32_t>> pc(ncol);
+    std::vector<int> lo(ncol, 1 << 30), hi(ncol, -1);
+    for (int64_t id = (int64_t)(v0 - 1) * layer_patches; id < (int64_t)v1 * layer_patches; ++id) {
+      int64_t rem = id;
+      int v[3] = {1, 1, 1}, parq = 0, half = 0;
+      for (int t = 0; t < d; ++t) {
+        v[t] = 1 + (int)(rem % (nc[t] - 1));
+        rem /= (nc[t] - 1);
+        parq += (v[t] & 1) << t;
+        half += v[t] / 2;
+      }
+      const int col = parq * 2 + (half & 1);
+      pc[col].push_back(pack3(v[0], v[1], d == 3 ? v[2] : 0));
+      lo[col] = std::min(lo[col], v[d - 1] - 1);
+      hi[col] = std::max(hi[col], v[d - 1]);
+    }
+    for (int c = 0; c < ncol; ++c) {
+      if (pc[c].empty()) continue;
+      HT t{1, c, blk, lo[c], hi[c], (int64_t)plist.size(), (int64_t)pc[c].size(),
+           (double)c + (double)skew * blk, {}};
+      plist.insert(plist.end(), pc[c].begin(), pc[c].end());
+      ptasks.push_back(t);
+    }
+  }
+  std::stable_sort(ptasks.begin(), ptasks.end(), [](const HT& a, const HT& b) {
+    return a.key < b.key || (a.key == b.key && a.blk < b.blk);
+  });
+  // residual layers, each inserted right before the first patch task that
+  // reads its r or writes the x it reads
+  std::vector<std::vector<HT>> before(ptasks.size() + 1);
+  for (int z = L->desc.res_begin; z < L->desc.res_end; ++z) {
+    size_t pos = ptasks.size();
+    for (size_t i = 0; i < ptasks.size(); ++i)
+      if (ptasks[i].hi >= z - 1 && ptasks[i].lo <= z + 1) { pos = i; break; }
+    HT r{0, -1, -1, z - 1, z + 1, (int64_t)(z - zb) * L->layer_cells, L->layer_cells, 0.0, {}};
+    if (pos == ptasks.size()) before[0].push_back(r);
+    else before[pos].push_back(r);
+  }
+  std::vector<HT> seq;
+  for (size_t i = 0; i <= ptasks.size(); ++i) {
+    for (auto& r : before[i]) seq.push_back(r);
+    if (i < ptasks.size()) seq.push_back(ptasks[i]);
+  }
+  const int nt = (int)seq.size();
+  // dependencies (conflicting earlier tasks), transitively reduced
+  const int words = (nt + 63) / 64;
+  std::vector<std::vector<uint64_t>> anc(nt, std::vector<uint64_t>(words, 0));
+  auto conflict = [](const HT& a, const HT& b) {
+    if (a.type == 0 && b.type == 0) return false;
+    if (a.type == 1 && b.type == 1)
+      return a.colour != b.colour && a.hi >= b.lo && b.hi >= a.lo;
+    return a.hi >= b.lo && b.hi >= a.lo;  // R(z) vs P: x/r layer overlap
+  };
+  for (int j = 0; j < nt; ++j) {
+    for (int i = j - 1; i >= 0; --i) {
+      if (!conflict(seq[i], seq[j])) continue;
+      if (seq[j].type == 0) return fail(DG_EINVAL, "flow: residual after a conflicting patch task");
+      if (anc[j][i / 64] >> (i % 64) & 1) continue;  // implied by a kept dependency
+      seq[j].deps.push_back(i);
+      anc[j][i / 64] |= uint64_t(1) << (i % 64);
+      for (int w = 0; w < words; ++w) anc[j][w] |= anc[i][w];
+    }
+    if ((int)seq[j].deps.size() > FLOW_MAX_DEPS) return DG_OK;  // keep colour launches
+  }
+  std::vector<FlowTask> ht(nt);
+  std::vector<int32_t> item_task;
+  for (int j = 0; j < nt; ++j) {
+    FlowTask& t = ht[j];
+    const int g = seq[j].type == 0 ? gr : gp;
+    t.type = seq[j].type;
+    t.units = (int)((seq[j].count + g - 1) / g);
+    t.first_item = (int64_t)item_task.size();
+    t.start = seq[j].start;
+    t.count = seq[j].count;
+    t.ndeps = (int)seq[j].deps.size();
+    for (int i = 0; i < FLOW_MAX_DEPS; ++i) t.deps[i] = i < t.ndeps ? seq[j].deps[i] : -1;
+    if (env_int("DGB_FLOW_NODEPS", 0)) t.ndeps = 0;  // timing experiment only (wrong results)
+    item_task.insert(item_task.end(), t.units, j);
+  }
+  FlowDev& f = L->flow;
+  DG_CUDA(cudaMalloc(&f.tasks, sizeof(FlowTask) * nt));
+  DG_CUDA(cudaMemcpy(f.tasks, ht.data(), sizeof(FlowTask) * nt, cudaMemcpyHostToDevice));
+  DG_CUDA(cudaMalloc(&f.item_task, sizeof(int32_t) * item_task.size()));
+  DG_CUDA(cudaMemcpy(f.item_task, item_task.data(), sizeof(int32_t) * item_task.size(),
+                     cudaMemcpyHostToDevice));
+  DG_CUDA(cudaMalloc(&f.plist, sizeof(int32_t) * std::max<size_t>(1, plist.size())));
+  if (!plist.empty())
+    DG_CUDA(cudaMemcpy(f.plist, plist.data(), sizeof(int32_t) * plist.size(), cudaMemcpyHostToDevice));
+  DG_CUDA(cudaMalloc(&f.ctrl, sizeof(unsigned) * (1 + nt)));
+  f.ntasks = nt;
+  f.nitems = (int64_t)item_task.size();
+  L->flow_ok = true;
   return DG_OK;
 }
 
@@ -317,6 +578,10 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   L->geo.nc[2] = d == 3 ? desc->ncells[2] : 1;
   L->geo.zb = desc->z_begin;
   L->geo.zn = desc->z_count;
+  for (int t = 0; t < 3; ++t) {
+    L->geo.fc[t].init((uint32_t)L->geo.nc[t]);
+    L->geo.fv[t].init((uint32_t)std::max(1, L->geo.nc[t] - 1));
+  }
   L->alpha = T->alpha;
   L->beta = T->beta;
   L->betap = T->betap;
@@ -384,24 +649,28 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   };
   // red-black over owned cells (mesh.py:350-357), ascending local ids
   {
-    std::vector<int32_t> col[2];
+    std::vector<int32_t> col[2], colp[2];
     const int64_t c0 = (int64_t)(desc->own_begin - zb) * L->layer_cells;
     const int64_t c1 = (int64_t)(desc->own_end - zb) * L->layer_cells;
     for (int64_t id = c0; id < c1; ++id) {
       int64_t rem = id;
-      int s = 0;
+      int s = 0, cc3[3] = {0, 0, 0};
       for (int t = 0; t < d; ++t) {
         const int64_t ct = (t == d - 1) ? rem + zb : rem % nc[t];
         rem /= nc[t];
         s += (int)ct;
+        cc3[t] = (int)ct;
       }
       col[s & 1].push_back((int32_t)id);
+      colp[s & 1].push_back(pack3(cc3[0], cc3[1], cc3[2]));
     }
     for (int k = 0; k < 2; ++k) {
       if (col[k].empty()) continue;
-      DevList dl;
+      DevList dl, dp;
       int rc = upload_list(col[k], &dl);
       L->rb.push_back(dl);
+      if (!rc) rc = upload_list(colp[k], &dp);
+      L->rb_pk.push_back(dp);
       if (rc) { free_level(L); return rc; }
     }
   }
@@ -409,7 +678,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   // [pv_begin, pv_end]; ids ascending inside each colour
   if (L->has_patch) {
     const int ncol = 1 << (d + 1);
-    std::vector<std::vector<int32_t>> pc(ncol), cc(ncol);
+    std::vector<std::vector<int32_t>> pc(ncol), cc(ncol), pcp(ncol), ccp(ncol);
     bool ok = true;
     for (int t = 0; t < d; ++t) ok = ok && nc[t] >= 2;
     const int vlo = std::max(1, desc->pv_begin), vhi = std::min(nc[d - 1] - 1, desc->pv_end);
@@ -432,20 +701,26 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
         }
         const int col = parq * 2 + (half & 1);
         pc[col].push_back((int32_t)id);
+        pcp[col].push_back(pack3(v[0], v[1], d == 3 ? v[2] : 0));
         for (int s = 0; s < (1 << d); ++s) {
           int c[3] = {0, 0, 0};
           for (int t = 0; t < d; ++t) c[t] = v[t] - 1 + ((s >> t) & 1);
           cc[col].push_back(local_of(c));
+          ccp[col].push_back(pack3(c[0], c[1], c[2]));
         }
       }
     }
     for (int k = 0; k < ncol; ++k) {
       if (pc[k].empty()) continue;
-      DevList a, b;
+      DevList a, b, ap, bp;
       int rc = upload_list(pc[k], &a);
       L->pcol.push_back(a);
       if (!rc) rc = upload_list(cc[k], &b);
       L->pcol_cells.push_back(b);
+      if (!rc) rc = upload_list(pcp[k], &ap);
+      L->pcol_pk.push_back(ap);
+      if (!rc) rc = upload_list(ccp[k], &bp);
+      L->pcol_cells_pk.push_back(bp);
       if (rc) { free_level(L); return rc; }
     }
   }
@@ -455,6 +730,10 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     return fail(DG_EINVAL, "owned layers outside the window");
   }
   if (int rc = check_layers(L, desc->res_begin, desc->res_end)) {
+    free_level(L);
+    return rc;
+  }
+  if (int rc = build_flow(L)) {
     free_level(L);
     return rc;
   }
@@ -479,7 +758,7 @@ int dg_apply(const dg_level_t* L, const double* u, double* v, int z0, int z1, vo
   if (u == v) return fail(DG_EINVAL, "apply_operator: output must not alias input");
   if (int rc = check_layers(L, z0, z1)) return rc;
   if (int rc = check_align(L, u, v, nullptr)) return rc;
-  ResParams p = res_params(L, u, nullptr, v);
+  ResArgs p = res_params(L, u, nullptr, v);
   p.start = (int64_t)(z0 - L->desc.z_begin) * L->layer_cells;
   p.count = (int64_t)(z1 - z0) * L->layer_cells;
   return dispatch_residual(L->d, L->n, p, L->hres(), (cudaStream_t)stream);
@@ -491,7 +770,7 @@ int dg_residual(const dg_level_t* L, const double* x, const double* b, double* r
   if (r == x) return fail(DG_EINVAL, "residual: output must not alias x");
   if (int rc = check_layers(L, z0, z1)) return rc;
   if (int rc = check_align(L, x, b, r)) return rc;
-  ResParams p = res_params(L, x, b, r);
+  ResArgs p = res_params(L, x, b, r);
   p.start = (int64_t)(z0 - L->desc.z_begin) * L->layer_cells;
   p.count = (int64_t)(z1 - z0) * L->layer_cells;
   return dispatch_residual(L->d, L->n, p, L->hres(), (cudaStream_t)stream);
@@ -502,7 +781,7 @@ int dg_residual_cells(const dg_level_t* L, const double* x, const double* b, dou
   if (!L || !x || !b || !r || (!cells && n_cells > 0)) return fail(DG_EINVAL, "null argument");
   if (r == x) return fail(DG_EINVAL, "residual: output must not alias x");
   if (int rc = check_align(L, x, b, r)) return rc;
-  ResParams p = res_params(L, x, b, r);
+  ResArgs p = res_params(L, x, b, r);
   p.list = cells;
   p.count = n_cells;
   return dispatch_residual(L->d, L->n, p, L->hres(), (cudaStream_t)stream);
@@ -513,7 +792,7 @@ int dg_cell_fdm(const dg_level_t* L, const double* r, double* x, double omega,
   if (!L || !r || !x) return fail(DG_EINVAL, "null argument");
   if (r == x) return fail(DG_EINVAL, "cell solve: r must not alias x");
   if (int rc = check_align(L, r, x, nullptr)) return rc;
-  FdmParams p = fdm_params(L, false, r, x, omega);
+  FdmArgs p = fdm_params(L, false, r, x, omega);
   if (cells) {
     p.list = cells;
     p.count = n_cells;
@@ -531,7 +810,7 @@ int dg_patch_fdm(const dg_level_t* L, const double* r, double* x, double omega,
   if (int rc = check_align(L, r, x, nullptr)) return rc;
   if (!L->has_patch)
     return fail(DG_EUNSUPPORTED, "vertex-patch tables not available (degree > 7?)");
-  FdmParams p = fdm_params(L, true, r, x, omega);
+  FdmArgs p = fdm_params(L, true, r, x, omega);
   p.list = patches;
   p.count = n_patches;
   p.atomic = atomic;
@@ -579,12 +858,40 @@ int dg_patch_gather_map(const dg_level_t* L, const int32_t* patches, int64_t cou
   return DG_OK;
 }
 
+// internal launches over the level's packed colour lists (no index division)
+static int res_packed(dg_level_t* L, const double* x, const double* b, double* r,
+                      const DevList& l, cudaStream_t st) {
+  ResArgs p = res_params(L, x, b, r);
+  p.list = l.ptr;
+  p.count = l.count;
+  p.packed = 1;
+  return dispatch_residual(L->d, L->n, p, L->hres(), st);
+}
+
+static int cell_fdm_packed(dg_level_t* L, const double* r, double* x, double omega,
+                           const DevList& l, cudaStream_t st) {
+  FdmArgs p = fdm_params(L, false, r, x, omega);
+  p.list = l.ptr;
+  p.count = l.count;
+  p.packed = 1;
+  return dispatch_cell_fdm(L->d, L->n, p, L->hcz.data(), L->hczt.data(), st);
+}
+
+static int patch_fdm_packed(dg_level_t* L, const double* r, double* x, double omega,
+                            const DevList& l, cudaStream_t st) {
+  FdmArgs p = fdm_params(L, true, r, x, omega);
+  p.list = l.ptr;
+  p.count = l.count;
+  p.packed = 1;
+  return dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), st);
+}
+
 static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, double* x,
                            const double* b, double* r, cudaStream_t st, int64_t* nl) {
   int rc = DG_OK;
   *nl = 0;
   auto res_range = [&]() {
-    ResParams p = res_params(L, x, b, r);
+    ResArgs p = res_params(L, x, b, r);
     p.start = (int64_t)(L->desc.res_begin - L->desc.z_begin) * L->layer_cells;
     p.count = (int64_t)(L->desc.res_end - L->desc.res_begin) * L->layer_cells;
     ++*nl;
@@ -598,33 +905,38 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
     }
     case DG_AVS: {
       if (!L->has_patch) return fail(DG_EUNSUPPORTED, "vertex patches unsupported here");
-      if ((rc = res_range())) return rc;
-      for (auto& c : L->pcol) {
+      if (L->flow_ok && env_int("DGB_FLOW", 0)) {
         ++*nl;
-        if ((rc = dg_patch_fdm(L, r, x, omega, c.ptr, c.count, 0, st))) return rc;
+        ResArgs ra = res_params(L, x, b, r);
+        FdmArgs fa = fdm_params(L, true, r, x, omega);
+        return dispatch_flow(L->d, L->n, ra, fa, L->hres(), L->hpz.data(), L->hpzt.data(),
+                             L->flow, st);
+      }
+      if ((rc = res_range())) return rc;
+      for (auto& c : L->pcol_pk) {
+        ++*nl;
+        if ((rc = patch_fdm_packed(L, r, x, omega, c, st))) return rc;
       }
       return DG_OK;
     }
     case DG_MCS: {
-      const int nc = (int)L->rb.size();
+      const int nc = (int)L->rb_pk.size();
       for (int i = 0; i < nc; ++i) {
-        const auto& c = L->rb[reverse ? nc - 1 - i : i];
+        const auto& c = L->rb_pk[reverse ? nc - 1 - i : i];
         *nl += 2;
-        if ((rc = dg_residual_cells(L, x, b, r, c.ptr, c.count, st))) return rc;
-        if ((rc = dg_cell_fdm(L, r, x, omega, c.ptr, c.count, st))) return rc;
+        if ((rc = res_packed(L, x, b, r, c, st))) return rc;
+        if ((rc = cell_fdm_packed(L, r, x, omega, c, st))) return rc;
       }
       return DG_OK;
     }
     case DG_MVS: {
       if (!L->has_patch) return fail(DG_EUNSUPPORTED, "vertex patches unsupported here");
-      const int nc = (int)L->pcol.size();
+      const int nc = (int)L->pcol_pk.size();
       for (int i = 0; i < nc; ++i) {
         const int k = reverse ? nc - 1 - i : i;
         *nl += 2;
-        if ((rc = dg_residual_cells(L, x, b, r, L->pcol_cells[k].ptr, L->pcol_cells[k].count, st)))
-          return rc;
-        if ((rc = dg_patch_fdm(L, r, x, omega, L->pcol[k].ptr, L->pcol[k].count, 0, st)))
-          return rc;
+        if ((rc = res_packed(L, x, b, r, L->pcol_cells_pk[k], st))) return rc;
+        if ((rc = patch_fdm_packed(L, r, x, omega, L->pcol_pk[k], st))) return rc;
       }
       return DG_OK;
     }
@@ -667,5 +979,9 @@ int dg_smooth(dg_level_t* L, int kind, double omega, int reverse, double* x, con
 }
 
 int64_t dg_last_launch_count(const dg_level_t* L) { return L ? L->last_launches : -1; }
+
+int dg_flow_enabled(const dg_level_t* L) {
+  return L && L->flow_ok && env_int("DGB_FLOW", 0) ? 1 : 0;
+}
 
 }  // extern "C"

@@ -14,10 +14,13 @@
 //  - gather / scatter move whole cell rows (n contiguous doubles of one
 //    cell, 16-byte vectors when n is even) so index math is per row, not per
 //    element; a patch row lands at (s0 n, s1 n + i1, s2 n + i2) of the patch
-//    tensor (fastdiag.py:546-557);
+//    tensor (fastdiag.py:546-557); the update is a vectorised
+//    load-add-store (write-disjoint colours) or fp64 RED reductions when the
+//    caller asks for overlap-safe accumulation (measured: RED costs ~0.1 ms
+//    per cfg-5 colour at L2, so the disjoint path avoids it);
 //  - several subdomains per CTA so that the CTA is a whole number of warps.
 #pragma once
-#include "kernels.cuh"
+#include "common.cuh"
 
 namespace dgb {
 
@@ -28,14 +31,6 @@ struct FdmMats {
 };
 
 template <int D, int M>
-__host__ __device__ constexpr int fdm2_groups() {
-  constexpr int F = Lay<D, M>::F;
-  for (int g = 1; g <= 32; ++g)
-    if ((g * F) % 32 == 0 && g * F >= 128 && g * F <= 512) return g;
-  return F >= 128 ? 1 : (128 + F - 1) / F;
-}
-
-template <int D, int M>
 struct Fdm2Params {
   const double* r;
   double* x;
@@ -44,7 +39,8 @@ struct Fdm2Params {
   int64_t count;
   const double* invsum;
   double omega;
-  int atomic;
+  int atomic;   // overlapping subdomains: fp64 reductions instead of load-add-store
+  int packed;   // list entries are packed global coordinates (pack3)
   Geo geo;
   FdmMats<M> mats;
 };
@@ -123,6 +119,50 @@ __device__ __forceinline__ void row_update(double* __restrict__ g, const double*
   }
 }
 
+// L2-coherent variants (ld.global.cg) for data written by other CTAs of the
+// same kernel (dataflow kernel)
+template <int N>
+__device__ __forceinline__ void row_load_cg(double* __restrict__ s, const double* __restrict__ g) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(g + i));
+      s[i] = v.x;
+      s[i + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) s[i] = __ldcg(g + i);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void row_update_cg(double* __restrict__ g, const double* __restrict__ s,
+                                              double omega) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      double2 v = __ldcg(reinterpret_cast<const double2*>(g + i));
+      v.x = fma(omega, s[i], v.x);
+      v.y = fma(omega, s[i + 1], v.y);
+      __stcg(reinterpret_cast<double2*>(g + i), v);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) __stcg(g + i, fma(omega, s[i], __ldcg(g + i)));
+  }
+}
+
+// x[row] += omega * y as fp64 reductions at L2 (RED.E.ADD.F64, no load
+// latency on the SM).  Correct for overlapping subdomains too; within one
+// launch of a colour every DoF is hit once, so the result is deterministic.
+template <int N>
+__device__ __forceinline__ void row_red(double* __restrict__ g, const double* __restrict__ s,
+                                        double omega) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) atomicAdd(g + i, omega * s[i]);
+}
+
 template <int N>
 __device__ __forceinline__ void row_load_reg(double (&v)[N], const double* __restrict__ g) {
   if constexpr (N % 2 == 0) {
@@ -149,6 +189,14 @@ __device__ __forceinline__ void row_store(double* __restrict__ g, const double (
   }
 }
 
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
+
 // rows of a subdomain: (cell slot, i1, i2) -> (global offset, shared offset)
 template <int D, int M, bool PATCH>
 struct Rows {
@@ -168,28 +216,30 @@ struct Rows {
   }
 };
 
-template <int D, int M, bool PATCH>
-__global__ void __launch_bounds__(fdm2_groups<D, M>() * Lay<D, M>::F)
-fdm2_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
+// one group of G subdomains (work items grp*G .. grp*G+G-1); all G*F threads
+// of the CTA take part; `sm` holds G*SZ doubles.  `coherent` reads r and x
+// through L2 only (ld.cg) for use inside a kernel where other CTAs write them.
+template <int D, int M, bool PATCH, int G>
+__device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32_t* list,
+                                          int packed, int64_t start, int64_t count, int64_t grp,
+                                          double* sm, bool coherent) {
   using L = Lay<D, M>;
   using R = Rows<D, M, PATCH>;
   constexpr int N = R::N;
   constexpr int NEc = (D == 3) ? N * N * N : N * N;
-  constexpr int G = fdm2_groups<D, M>();
   constexpr int F = L::F;
   constexpr int NT = G * F;
-  extern __shared__ double sm[];
   __shared__ int s_info[G][8];            // digit[3], cls, active
   __shared__ int64_t s_cell[G][R::SLOTS];  // dof offset of each cell of the subdomain
   const int tid = threadIdx.x;
   if (tid < G) {
-    const int64_t idx = (int64_t)blockIdx.x * G + tid;
+    const int64_t idx = grp * G + tid;
     int* inf = s_info[tid];
-    inf[7] = idx < p.count;
+    inf[7] = idx < count;
     int digit[3] = {0, 0, 0}, base[3] = {0, 0, 0};
     if (inf[7]) {
-      const int id = p.list ? p.list[idx] : (int)(p.start + idx);
-      subdomain_info<D, PATCH>(p.geo, id, digit, base);
+      const int id = list ? list[idx] : (int)(start + idx);
+      subdomain_info<D, PATCH>(p.geo, id, packed != 0, digit, base);
     }
     int cls = 0;
 #pragma unroll
@@ -211,7 +261,8 @@ fdm2_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
     if (!s_info[g][7]) continue;
     int slot, goff, soff;
     R::map(row - g * R::RPS, slot, goff, soff);
-    row_load<N>(sm + g * L::SZ + soff, p.r + s_cell[g][slot] + goff);
+    if (coherent) row_load_cg<N>(sm + g * L::SZ + soff, p.r + s_cell[g][slot] + goff);
+    else row_load<N>(sm + g * L::SZ + soff, p.r + s_cell[g][slot] + goff);
   }
   __syncthreads();
   const int g = tid / F, f = tid - (tid / F) * F;
@@ -253,9 +304,20 @@ fdm2_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
     if (!s_info[gg][7]) continue;
     int slot, goff, soff;
     R::map(row - gg * R::RPS, slot, goff, soff);
-    row_update<N>(p.x + s_cell[gg][slot] + goff, sm + gg * L::SZ + soff, p.omega, p.atomic != 0);
+    if (p.atomic) row_red<N>(p.x + s_cell[gg][slot] + goff, sm + gg * L::SZ + soff, p.omega);
+    else if (coherent) row_update_cg<N>(p.x + s_cell[gg][slot] + goff, sm + gg * L::SZ + soff, p.omega);
+    else row_update<N>(p.x + s_cell[gg][slot] + goff, sm + gg * L::SZ + soff, p.omega, false);
   }
 }
+
+template <int D, int M, bool PATCH>
+__global__ void __launch_bounds__(fdm2_groups<D, M>() * Lay<D, M>::F)
+fdm2_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
+  extern __shared__ double sm[];
+  fdm_group<D, M, PATCH, fdm2_groups<D, M>()>(p, p.list, p.packed, p.start, p.count, blockIdx.x,
+                                              sm, false);
+}
+
 
 template <int D, int M>
 __host__ __device__ constexpr int fdm2_smem_doubles() {

@@ -17,7 +17,7 @@
 //   4: B <- M B   [t=1]
 //   5: A <- A + M B [t=0]; then r = b - A (coalesced)
 #pragma once
-#include "kernels.cuh"
+#include "common.cuh"
 #include "fdm2.cuh"
 
 namespace dgb {
@@ -39,9 +39,32 @@ struct Res2Params {
   int64_t start;
   int64_t count;
   double alpha, beta, betap;
+  int packed;   // list entries are packed global cell coordinates (pack3)
   Geo geo;
   ResMats<N> mats;
 };
+
+// cell of work item idx: local id (or -1) and global multi-index
+template <int D>
+__device__ __forceinline__ int res_cell(const Geo& geo, const int32_t* list, int packed,
+                                        int64_t start, int64_t count, int64_t idx, int* c) {
+  c[0] = c[1] = c[2] = 0;
+  if (idx >= count) return -1;
+  if (list) {
+    const int e = list[idx];
+    if (packed) {
+      c[0] = e & 1023;
+      c[1] = (e >> 10) & 1023;
+      c[2] = (e >> 20) & 1023;
+      return cell_local<D>(geo, c);
+    }
+    cell_multi<D>(geo, e, c);
+    return e;
+  }
+  const int cell = (int)(start + idx);
+  cell_multi<D>(geo, cell, c);
+  return cell;
+}
 
 // G_t fiber: A_diag(digit) along t plus the rank-2 neighbour couplings
 template <int D, int N>
@@ -106,20 +129,19 @@ __device__ __forceinline__ void mass_fiber(const Res2Params<D, N>& p, int t, int
   for (int k = 0; k < N; ++k) buf[sb + k * ss] = o[k];
 }
 
-template <int D, int N>
-__global__ void __launch_bounds__(fdm2_groups<D, N>() * Lay<D, N>::F)
-res2_kernel(const __grid_constant__ Res2Params<D, N> p) {
+// one group of G cells (work items grp*G .. grp*G+G-1 of the list/range);
+// all NT = G*F threads of the CTA take part; `sm` holds 3*G*SZ doubles.
+template <int D, int N, int G>
+__device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32_t* list,
+                                          int packed, int64_t start, int64_t count, int64_t grp,
+                                          double* sm) {
   using L = Lay<D, N>;
-  constexpr int G = fdm2_groups<D, N>();
   constexpr int F = L::F;
   constexpr int NT = G * F;
-  extern __shared__ double sm[];
   __shared__ int s_cell[G];
+  __shared__ int s_c[G][3];
   const int tid = threadIdx.x;
-  if (tid < G) {
-    const int64_t idx = (int64_t)blockIdx.x * G + tid;
-    s_cell[tid] = idx < p.count ? (p.list ? p.list[idx] : (int)(p.start + idx)) : -1;
-  }
+  if (tid < G) s_cell[tid] = res_cell<D>(p.geo, list, packed, start, count, grp * G + tid, s_c[tid]);
   __syncthreads();
   using R = Rows<D, N, false>;
   for (int row = tid; row < G * R::RPS; row += NT) {
@@ -133,8 +155,7 @@ res2_kernel(const __grid_constant__ Res2Params<D, N> p) {
   const int g = tid / F, f = tid - (tid / F) * F;
   const int cell = s_cell[g];
   const bool active = cell >= 0;
-  int c[3] = {0, 0, 0};
-  cell_multi<D>(p.geo, active ? cell : 0, c);
+  const int c[3] = {s_c[g][0], s_c[g][1], s_c[g][2]};
   double* X = sm + g * L::SZ;
   double* A = sm + (G + g) * L::SZ;
   double* B = sm + (2 * G + g) * L::SZ;
@@ -197,6 +218,14 @@ res2_kernel(const __grid_constant__ Res2Params<D, N> p) {
     }
   }
 }
+
+template <int D, int N>
+__global__ void __launch_bounds__(fdm2_groups<D, N>() * Lay<D, N>::F)
+res2_kernel(const __grid_constant__ Res2Params<D, N> p) {
+  extern __shared__ double sm[];
+  res_group<D, N, fdm2_groups<D, N>()>(p, p.list, p.packed, p.start, p.count, blockIdx.x, sm);
+}
+
 
 template <int D, int N>
 __host__ __device__ constexpr int res2_smem_doubles() {

@@ -256,3 +256,22 @@ def test_unsupported_patch_degree_raises():
     ctx = dg.make_context(lvl, basis)
     with pytest.raises(NotImplementedError):
         dg.make_level_smoother(ctx, basis, dg.SmootherConfig("avs", 0.25))
+
+
+@pytest.mark.parametrize("d,nc,k", [(3, 12, 3), (3, 10, 5), (2, 20, 4), (3, 9, 7)])
+def test_dataflow_avs_kernel_bitwise_equals_colour_launches(d, nc, k, monkeypatch):
+    """The persistent dataflow AVS kernel (DGB_FLOW=1, flow.cuh) reorders the
+    work across z-blocks but keeps every DoF's colour order: bit-identical."""
+    ctx, _, sm = _setup(d, nc, k, "avs", 0.25)
+    x0, b = inputs(ctx.ndofs, 6)
+    monkeypatch.setenv("DGB_FLOW", "0")
+    xa = x0.copy()
+    sm.smooth(xa, b)
+    monkeypatch.setenv("DGB_FLOW", "1")
+    assert ctx.dev._lib.dg_flow_enabled(ctx.dev.handle) == 1
+    xb = x0.copy()
+    sm.use_graph = False
+    sm.smooth(xb, b)
+    assert np.array_equal(xa, xb)
+    want = OracleLevel((nc,) * d, k).smooth("avs", 0.25, x0, b)
+    assert rel(xb, want) <= RTOL
