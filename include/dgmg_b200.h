@@ -75,6 +75,15 @@ typedef struct dg_tables {
   const double* patch_z;       /* 4*m*m    patch eigenvectors, m = 2n (or NULL)*/
   const double* patch_zt;      /* 4*m*m                                        */
   const double* patch_invsum;  /* 4^d*m^d                                      */
+  /* even/odd factorisation of the interior digit (NULL = dense everywhere):
+   * the interior eigenpairs in cell_z/patch_z (and the class 1/Lambda tables)
+   * must be ordered even-first; halves are (s/2)x(s/2), k-outer row-major:
+   * *_eo = [Z_top_even, Z_top_odd, Z_top_even^T, Z_top_odd^T],
+   * res_eo = [P^T, Q^T of M, P^T, Q^T of A_diag(0)] with
+   * P = (A11 + A12 J)/2, Q = (A11 - A12 J)/2 (centro-symmetric splitting). */
+  const double* cell_eo;       /* 4*(n/2)^2 or NULL                           */
+  const double* patch_eo;      /* 4*(m/2)^2 or NULL                           */
+  const double* res_eo;        /* 4*(n/2)^2 or NULL                           */
 } dg_tables_t;
 
 typedef struct dg_level dg_level_t;

@@ -12,7 +12,7 @@ import os
 
 import numpy as np
 
-from .tables import LevelTables, SingularLocalSolverError
+from .tables import LevelTables, SingularLocalSolverError, device_tables
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdgmg_b200.so")
@@ -50,7 +50,8 @@ class Tables(ctypes.Structure):
                 ("alpha", ctypes.c_double), ("beta", ctypes.c_double),
                 ("betap", ctypes.c_double), ("cell_z", _dp), ("cell_zt", _dp),
                 ("cell_invsum", _dp), ("patch_z", _dp), ("patch_zt", _dp),
-                ("patch_invsum", _dp)]
+                ("patch_invsum", _dp), ("cell_eo", _dp), ("patch_eo", _dp),
+                ("res_eo", _dp)]
 
 
 _lib = None
@@ -117,8 +118,10 @@ class DeviceLevel:
                  z_begin: int = 0, z_count: int | None = None,
                  own: tuple[int, int] | None = None,
                  res: tuple[int, int] | None = None,
-                 pv: tuple[int, int] | None = None):
+                 pv: tuple[int, int] | None = None, use_eo: bool | None = None):
         lib = load()
+        if use_eo is None:
+            use_eo = os.environ.get("DGB_EO", "1") != "0"
         d = tables.dim
         last = dims[-1]
         z_count = last - z_begin if z_count is None else z_count
@@ -143,18 +146,24 @@ class DeviceLevel:
             keep.append(c)
             return _ptr(c)
 
+        dt = device_tables(tables, tuple(dims), use_eo=use_eo)
         t = Tables()
         t.mass = arr(tables.mass)
         t.adiag = arr(tables.adiag)
         t.bg = arr(tables.bg)
         t.alpha, t.beta, t.betap = tables.alpha, tables.beta, tables.betap
-        t.cell_z = arr(tables.cell_z)
-        t.cell_zt = arr(np.transpose(tables.cell_z, (0, 2, 1)))
-        t.cell_invsum = arr(tables.cell_invsum)
-        if tables.patch_z is not None and tables.n <= 8:
-            t.patch_z = arr(tables.patch_z)
-            t.patch_zt = arr(np.transpose(tables.patch_z, (0, 2, 1)))
-            t.patch_invsum = arr(tables.patch_invsum)
+        t.cell_z = arr(dt.cell_z)
+        t.cell_zt = arr(np.transpose(dt.cell_z, (0, 2, 1)))
+        t.cell_invsum = arr(dt.cell_invsum)
+        t.cell_eo = arr(dt.cell_eo)
+        t.res_eo = arr(dt.res_eo)
+        if dt.patch_z is not None and tables.n <= 8:
+            t.patch_z = arr(dt.patch_z)
+            t.patch_zt = arr(np.transpose(dt.patch_z, (0, 2, 1)))
+            t.patch_invsum = arr(dt.patch_invsum)
+            t.patch_eo = arr(dt.patch_eo)
+        self.eo = {"cell": dt.cell_eo is not None, "patch": dt.patch_eo is not None,
+                   "residual": dt.res_eo is not None}
         h = ctypes.c_void_p()
         check(lib.dg_level_create(ctypes.byref(desc), ctypes.byref(t), ctypes.byref(h)))
         self._lib = lib

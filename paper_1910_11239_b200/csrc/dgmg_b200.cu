@@ -110,6 +110,7 @@ struct HostRes {
   const double* mass;   // n*n
   const double* adiag;  // 4*n*n
   const double* bg;     // 2*n
+  const double* eo;     // 4*(n/2)^2 or nullptr
 };
 
 template <int D, int N>
@@ -136,6 +137,8 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
     }
   std::memcpy(p.mats.bg0, h.bg, sizeof(p.mats.bg0));
   std::memcpy(p.mats.bg1, h.bg + N, sizeof(p.mats.bg1));
+  p.eo = h.eo != nullptr && N % 2 == 0;
+  if (p.eo) std::memcpy(p.mats.eo, h.eo, sizeof(p.mats.eo));
   const int64_t ngroups = (q.count + G - 1) / G;
   const size_t smem = sizeof(double) * res2_smem_doubles<D, N>();
   auto k = res2_kernel<D, N>;
@@ -150,16 +153,10 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
 }
 
 template <int D, int M, bool PATCH>
-static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, cudaStream_t st) {
+static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, const double* heo,
+                      cudaStream_t st) {
   if (q.count <= 0) return DG_OK;
   constexpr int G = fdm2_groups<D, M>();
-  const size_t smem = sizeof(double) * fdm2_smem_doubles<D, M>();
-  auto k = fdm2_kernel<D, M, PATCH>;
-  static bool attr = false;
-  if (!attr) {
-    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
   Fdm2Params<D, M> p;
   p.r = q.r;
   p.x = q.x;
@@ -174,8 +171,17 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, cud
   // fwd[k][i] = Z[k][i] (out = Z^T v); bwd[k][i] = Z^T[k][i] (out = Z v)
   std::memcpy(p.mats.fwd, hz, sizeof(p.mats.fwd));
   std::memcpy(p.mats.bwd, hzt, sizeof(p.mats.bwd));
-  const int64_t grid = (q.count + G - 1) / G;
-  k<<<(unsigned)grid, G * Lay<D, M>::F, smem, st>>>(p);
+  p.eo = heo != nullptr && M % 2 == 0;
+  if (p.eo) std::memcpy(p.mats.eo, heo, sizeof(p.mats.eo));
+  const int64_t ngroups = (q.count + G - 1) / G;
+  const size_t smem = sizeof(double) * fdm2_smem_doubles<D, M>();
+  auto k = fdm2_kernel<D, M, PATCH>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k<<<(unsigned)ngroups, G * Lay<D, M>::F, smem, st>>>(p);
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }
@@ -191,7 +197,7 @@ struct FlowDev {
 
 template <int D, int N>
 static int launch_flow(const ResArgs& ra, const FdmArgs& fa, const HostRes& h, const double* hz,
-                       const double* hzt, const FlowDev& fd, cudaStream_t st) {
+                       const double* hzt, const double* heo, const FlowDev& fd, cudaStream_t st) {
   using S = FlowShape<D, N>;
   constexpr int M = 2 * N;
   const size_t smem = sizeof(double) * S::SMEM;
@@ -221,6 +227,8 @@ static int launch_flow(const ResArgs& ra, const FdmArgs& fa, const HostRes& h, c
     }
   std::memcpy(r.mats.bg0, h.bg, sizeof(r.mats.bg0));
   std::memcpy(r.mats.bg1, h.bg + N, sizeof(r.mats.bg1));
+  r.eo = h.eo != nullptr && N % 2 == 0;
+  if (r.eo) std::memcpy(r.mats.eo, h.eo, sizeof(r.mats.eo));
   Fdm2Params<D, M>& f = p.fdm;
   f.r = fa.r;
   f.x = fa.x;
@@ -234,6 +242,8 @@ static int launch_flow(const ResArgs& ra, const FdmArgs& fa, const HostRes& h, c
   f.geo = fa.geo;
   std::memcpy(f.mats.fwd, hz, sizeof(f.mats.fwd));
   std::memcpy(f.mats.bwd, hzt, sizeof(f.mats.bwd));
+  f.eo = heo != nullptr;
+  if (f.eo) std::memcpy(f.mats.eo, heo, sizeof(f.mats.eo));
   p.tasks = fd.tasks;
   p.item_task = fd.item_task;
   p.plist = fd.plist;
@@ -255,8 +265,9 @@ static bool flow_shape(int d, int n, int* gp, int* gr) {
 }
 
 static int dispatch_flow(int d, int n, const ResArgs& ra, const FdmArgs& fa, const HostRes& h,
-                         const double* hz, const double* hzt, const FlowDev& fd, cudaStream_t st) {
-#define X(D, N) if (d == D && n == N) return launch_flow<D, N>(ra, fa, h, hz, hzt, fd, st);
+                         const double* hz, const double* hzt, const double* heo,
+                         const FlowDev& fd, cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_flow<D, N>(ra, fa, h, hz, hzt, heo, fd, st);
   X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
   X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 6) X(3, 7) X(3, 8)
 #undef X
@@ -278,8 +289,8 @@ static int dispatch_residual(int d, int n, const ResArgs& p, const HostRes& h,
 }
 
 static int dispatch_cell_fdm(int d, int n, const FdmArgs& p, const double* hz,
-                             const double* hzt, cudaStream_t st) {
-#define X(D, N) if (d == D && n == N) return launch_fdm<D, N, false>(p, hz, hzt, st);
+                             const double* hzt, const double* heo, cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_fdm<D, N, false>(p, hz, hzt, heo, st);
   DG_N_CASES(X, 2)
   DG_N_CASES(X, 3)
 #undef X
@@ -288,8 +299,8 @@ static int dispatch_cell_fdm(int d, int n, const FdmArgs& p, const double* hz,
 }
 
 static int dispatch_patch_fdm(int d, int n, const FdmArgs& p, const double* hz,
-                              const double* hzt, cudaStream_t st) {
-#define X(D, N) if (d == D && n == N) return launch_fdm<D, 2 * N, true>(p, hz, hzt, st);
+                              const double* hzt, const double* heo, cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_fdm<D, 2 * N, true>(p, hz, hzt, heo, st);
   X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
   X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 6) X(3, 7) X(3, 8)
 #undef X
@@ -332,8 +343,12 @@ struct dg_level {
   double alpha = 0, beta = 0, betap = 0;
   bool has_patch = false;
   std::vector<double> hcz, hczt, hpz, hpzt;  // host copies for the kernel parameter space
-  std::vector<double> hmass, hadiag, hbg;
-  HostRes hres() const { return HostRes{hmass.data(), hadiag.data(), hbg.data()}; }
+  std::vector<double> hmass, hadiag, hbg, hceo, hpeo, hreo;  // *_eo empty = dense path
+  HostRes hres() const {
+    return HostRes{hmass.data(), hadiag.data(), hbg.data(), hreo.empty() ? nullptr : hreo.data()};
+  }
+  const double* ceo() const { return hceo.empty() ? nullptr : hceo.data(); }
+  const double* peo() const { return hpeo.empty() ? nullptr : hpeo.data(); }
   std::vector<DevList> rb;          // red-black owned cells (MCS), local ids
   std::vector<DevList> rb_pk;       // same, packed global coordinates
   std::vector<DevList> pcol;        // patch colours (AVS / MVS), global patch ids
@@ -589,11 +604,14 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   L->hmass.assign(T->mass, T->mass + n * n);
   L->hadiag.assign(T->adiag, T->adiag + 4 * n * n);
   L->hbg.assign(T->bg, T->bg + 2 * n);
+  if (T->cell_eo && n % 2 == 0) L->hceo.assign(T->cell_eo, T->cell_eo + n * n);
+  if (T->res_eo && n % 2 == 0) L->hreo.assign(T->res_eo, T->res_eo + n * n);
   L->hcz.assign(T->cell_z, T->cell_z + 4 * n * n);
   L->hczt.assign(T->cell_zt, T->cell_zt + 4 * n * n);
   if (L->has_patch) {
     L->hpz.assign(T->patch_z, T->patch_z + 16 * n * n);
     L->hpzt.assign(T->patch_zt, T->patch_zt + 16 * n * n);
+    if (T->patch_eo) L->hpeo.assign(T->patch_eo, T->patch_eo + 4 * n * n);
   }
   const int m = L->m;
   const int64_t pw = (d == 3) ? 64 : 16;  // 4^d classes
@@ -800,7 +818,7 @@ int dg_cell_fdm(const dg_level_t* L, const double* r, double* x, double omega,
     p.start = (int64_t)(L->desc.own_begin - L->desc.z_begin) * L->layer_cells;
     p.count = (int64_t)(L->desc.own_end - L->desc.own_begin) * L->layer_cells;
   }
-  return dispatch_cell_fdm(L->d, L->n, p, L->hcz.data(), L->hczt.data(), (cudaStream_t)stream);
+  return dispatch_cell_fdm(L->d, L->n, p, L->hcz.data(), L->hczt.data(), L->ceo(), (cudaStream_t)stream);
 }
 
 int dg_patch_fdm(const dg_level_t* L, const double* r, double* x, double omega,
@@ -814,7 +832,7 @@ int dg_patch_fdm(const dg_level_t* L, const double* r, double* x, double omega,
   p.list = patches;
   p.count = n_patches;
   p.atomic = atomic;
-  return dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), (cudaStream_t)stream);
+  return dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), L->peo(), (cudaStream_t)stream);
 }
 
 int dg_num_colours(const dg_level_t* L, int kind) {
@@ -874,7 +892,7 @@ static int cell_fdm_packed(dg_level_t* L, const double* r, double* x, double ome
   p.list = l.ptr;
   p.count = l.count;
   p.packed = 1;
-  return dispatch_cell_fdm(L->d, L->n, p, L->hcz.data(), L->hczt.data(), st);
+  return dispatch_cell_fdm(L->d, L->n, p, L->hcz.data(), L->hczt.data(), L->ceo(), st);
 }
 
 static int patch_fdm_packed(dg_level_t* L, const double* r, double* x, double omega,
@@ -883,7 +901,7 @@ static int patch_fdm_packed(dg_level_t* L, const double* r, double* x, double om
   p.list = l.ptr;
   p.count = l.count;
   p.packed = 1;
-  return dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), st);
+  return dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), L->peo(), st);
 }
 
 static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, double* x,
@@ -910,7 +928,7 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
         ResArgs ra = res_params(L, x, b, r);
         FdmArgs fa = fdm_params(L, true, r, x, omega);
         return dispatch_flow(L->d, L->n, ra, fa, L->hres(), L->hpz.data(), L->hpzt.data(),
-                             L->flow, st);
+                             L->peo(), L->flow, st);
       }
       if ((rc = res_range())) return rc;
       for (auto& c : L->pcol_pk) {

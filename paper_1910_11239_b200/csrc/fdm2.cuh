@@ -28,6 +28,9 @@ template <int M>
 struct FdmMats {
   double fwd[4][M * M];  // Z per digit, row-major: fwd[k][i] = Z[k][i] -> out = Z^T v
   double bwd[4][M * M];  // Z^T per digit, row-major: bwd[k][i] = Z[i][k] -> out = Z v
+  // even/odd halves of the interior digit (tables.py device_tables):
+  // [0] top-even (k-outer fwd), [1] top-odd, [2] top-even^T, [3] top-odd^T
+  double eo[4][(M / 2) * (M / 2)];
 };
 
 template <int D, int M>
@@ -41,6 +44,7 @@ struct Fdm2Params {
   double omega;
   int atomic;   // overlapping subdomains: fp64 reductions instead of load-add-store
   int packed;   // list entries are packed global coordinates (pack3)
+  int eo;       // interior digit uses the even/odd halves
   Geo geo;
   FdmMats<M> mats;
 };
@@ -68,6 +72,118 @@ __device__ __forceinline__ void matvec_digit(const double (&S)[4][M * M], int di
     case 2: matvec_t<M>(S[2], v, o); break;
     default: matvec_t<M>(S[3], v, o); break;
   }
+}
+
+// even/odd split of an interior-digit contraction (half the FMAs):
+// forward  y_even = E^T u, y_odd = O^T w  with u = v_i + v_{m-1-i}, w = v_i - v_{m-1-i}
+// backward x_i = e_i + o_i, x_{m-1-i} = e_i - o_i, e = E y_even, o = O y_odd
+template <int M>
+__device__ __forceinline__ void matvec_eo_fwd(const double* __restrict__ E,
+                                              const double* __restrict__ O, const double (&v)[M],
+                                              double (&o)[M]) {
+  constexpr int H = M / 2;
+  double u[H], w[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    u[i] = v[i] + v[M - 1 - i];
+    w[i] = v[i] - v[M - 1 - i];
+  }
+#pragma unroll
+  for (int r = 0; r < H; ++r) {
+    o[r] = E[r] * u[0];
+    o[H + r] = O[r] * w[0];
+  }
+#pragma unroll
+  for (int k = 1; k < H; ++k) {
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+      o[r] = fma(E[k * H + r], u[k], o[r]);
+      o[H + r] = fma(O[k * H + r], w[k], o[H + r]);
+    }
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void matvec_eo_bwd(const double* __restrict__ Et,
+                                              const double* __restrict__ Ot, const double (&v)[M],
+                                              double (&o)[M]) {
+  constexpr int H = M / 2;
+  double e[H], q[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    e[i] = Et[i] * v[0];
+    q[i] = Ot[i] * v[H];
+  }
+#pragma unroll
+  for (int k = 1; k < H; ++k) {
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      e[i] = fma(Et[k * H + i], v[k], e[i]);
+      q[i] = fma(Ot[k * H + i], v[H + k], q[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    o[i] = e[i] + q[i];
+    o[M - 1 - i] = e[i] - q[i];
+  }
+}
+
+// centro-symmetric matrix (stored as k-outer P^T, Q^T halves): y = A v
+template <int M>
+__device__ __forceinline__ void matvec_cs(const double* __restrict__ Pt,
+                                          const double* __restrict__ Qt, const double (&v)[M],
+                                          double (&o)[M]) {
+  constexpr int H = M / 2;
+  double u[H], w[H], s[H], d[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    u[i] = v[i] + v[M - 1 - i];
+    w[i] = v[i] - v[M - 1 - i];
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    s[i] = Pt[i] * u[0];
+    d[i] = Qt[i] * w[0];
+  }
+#pragma unroll
+  for (int k = 1; k < H; ++k) {
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      s[i] = fma(Pt[k * H + i], u[k], s[i]);
+      d[i] = fma(Qt[k * H + i], w[k], d[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    o[i] = s[i] + d[i];
+    o[M - 1 - i] = s[i] - d[i];
+  }
+}
+
+// FDM contractions with the interior digit on the even/odd path
+template <int M, bool FWD>
+__device__ __forceinline__ void fdm_matvec(const FdmMats<M>& m, int eo, int digit,
+                                           const double (&v)[M], double (&o)[M]) {
+  if constexpr (M % 2 == 0) {
+    if (eo && digit == 0) {
+      if (FWD) matvec_eo_fwd<M>(m.eo[0], m.eo[1], v, o);
+      else matvec_eo_bwd<M>(m.eo[2], m.eo[3], v, o);
+      return;
+    }
+  }
+  matvec_digit<M>(FWD ? m.fwd : m.bwd, digit, v, o);
+}
+
+template <int M, bool FWD>
+__device__ __forceinline__ void fdm_fiber(const FdmMats<M>& m, int eo, int digit, double* buf,
+                                          int base, int stride) {
+  double v[M], o[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) v[k] = buf[base + k * stride];
+  fdm_matvec<M, FWD>(m, eo, digit, v, o);
+#pragma unroll
+  for (int k = 0; k < M; ++k) buf[base + k * stride] = o[k];
 }
 
 template <int M>
@@ -272,7 +388,7 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
   // forward contractions with Z^T, directions 0 .. D-2
 #pragma unroll
   for (int t = 0; t < D - 1; ++t) {
-    if (active) fiber_inplace<M>(p.mats.fwd, dg[t], buf, L::sbase(t, f), L::sstride(t));
+    if (active) fdm_fiber<M, true>(p.mats, p.eo, dg[t], buf, L::sbase(t, f), L::sstride(t));
     __syncthreads();
   }
   // fused: Z^T along D-1, scale by 1/Lambda-sum, Z along D-1
@@ -283,10 +399,10 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     double v[M], o[M];
 #pragma unroll
     for (int k = 0; k < M; ++k) v[k] = buf[sb + k * ss];
-    matvec_digit<M>(p.mats.fwd, dg[t], v, o);
+    fdm_matvec<M, true>(p.mats, p.eo, dg[t], v, o);
 #pragma unroll
     for (int k = 0; k < M; ++k) o[k] *= __ldg(inv + k * L::gstride(t));
-    matvec_digit<M>(p.mats.bwd, dg[t], o, v);
+    fdm_matvec<M, false>(p.mats, p.eo, dg[t], o, v);
 #pragma unroll
     for (int k = 0; k < M; ++k) buf[sb + k * ss] = v[k];
   }
@@ -295,7 +411,7 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
 #pragma unroll
   for (int s = 0; s < D - 1; ++s) {
     const int t = D - 2 - s;
-    if (active) fiber_inplace<M>(p.mats.bwd, dg[t], buf, L::sbase(t, f), L::sstride(t));
+    if (active) fdm_fiber<M, false>(p.mats, p.eo, dg[t], buf, L::sbase(t, f), L::sstride(t));
     __syncthreads();
   }
   // scatter-add omega * R_j^T y, one cell row per thread iteration

@@ -28,6 +28,8 @@ struct ResMats {
   double adiag[4][N * N];  // transposed A_diag per digit
   double bg0[N];
   double bg1[N];
+  // centro-symmetric halves (k-outer P^T, Q^T) of M and A_diag(0)
+  double eo[4][(N / 2) * (N / 2)];
 };
 
 template <int D, int N>
@@ -40,6 +42,7 @@ struct Res2Params {
   int64_t count;
   double alpha, beta, betap;
   int packed;   // list entries are packed global cell coordinates (pack3)
+  int eo;       // mass and interior stiffness on the even/odd path
   Geo geo;
   ResMats<N> mats;
 };
@@ -92,7 +95,12 @@ __device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, i
   double v[N], o[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) v[k] = X[sb + k * ss];
-  matvec_digit<N>(p.mats.adiag, digit, v, o);
+  if constexpr (N % 2 == 0) {
+    if (p.eo && digit == 0) matvec_cs<N>(p.mats.eo[2], p.mats.eo[3], v, o);
+    else matvec_digit<N>(p.mats.adiag, digit, v, o);
+  } else {
+    matvec_digit<N>(p.mats.adiag, digit, v, o);
+  }
   if (!(digit & 2)) {  // a_pm x_R: value and normal derivative at the shared face
     double g = 0.0;
 #pragma unroll
@@ -115,6 +123,18 @@ __device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, i
   for (int i = 0; i < N; ++i) out[sb + i * ss] = o[i];
 }
 
+template <int D, int N>
+__device__ __forceinline__ void res_mass(const Res2Params<D, N>& p, const double (&v)[N],
+                                         double (&o)[N]) {
+  if constexpr (N % 2 == 0) {
+    if (p.eo) {
+      matvec_cs<N>(p.mats.eo[0], p.mats.eo[1], v, o);
+      return;
+    }
+  }
+  matvec_t<N>(p.mats.mass, v, o);
+}
+
 // buf <- M buf along t (in place), optionally adding `add` first
 template <int D, int N, bool ADD>
 __device__ __forceinline__ void mass_fiber(const Res2Params<D, N>& p, int t, int f, double* buf,
@@ -124,7 +144,7 @@ __device__ __forceinline__ void mass_fiber(const Res2Params<D, N>& p, int t, int
   double v[N], o[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) v[k] = ADD ? buf[sb + k * ss] + add[sb + k * ss] : buf[sb + k * ss];
-  matvec_t<N>(p.mats.mass, v, o);
+  res_mass<D, N>(p, v, o);
 #pragma unroll
   for (int k = 0; k < N; ++k) buf[sb + k * ss] = o[k];
 }
@@ -183,7 +203,7 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
       double v[N], o[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) v[k] = B[sb + k];
-      matvec_t<N>(p.mats.mass, v, o);
+      res_mass<D, N>(p, v, o);
 #pragma unroll
       for (int k = 0; k < N; ++k) A[sb + k] += o[k];
     }

@@ -119,3 +119,52 @@ def step_work(kind: str, d: int, k: int, dims: tuple[int, ...]) -> tuple[float, 
             for v in dims:
                 kappa *= (v - 1) / v
     return kappa * fres + fsolve, kappa * 24.0 * ndofs
+
+
+def _contraction(m: int, eo: bool) -> float:
+    """flops of one length-m fiber contraction: dense m(2m-1); even/odd split
+    m^2 (two (m/2)^2 FMA blocks) + m (sums/differences or recombination)."""
+    return float(m * m + m) if eo else float(m * (2 * m - 1))
+
+
+def executed_step_flops(kind: str, d: int, k: int, dims: tuple[int, ...],
+                        eo_fdm: bool, eo_res: bool) -> float:
+    """Flops the device kernels execute for one step, counting the even/odd
+    split of interior-digit contractions (tables.device_tables) as used."""
+    n = k + 1
+    ncells = 1
+    for v in dims:
+        ncells *= v
+    fib = n ** (d - 1)
+    # residual per cell: d stiffness + (2d-1) mass contractions (3D: 3 + 5),
+    # rank-2 face couplings and the subtraction (SURVEY 8(d) convention)
+    nmass = 5 if d == 3 else 2
+    res = 0.0
+    for t in range(d):
+        inter = max(0, dims[t] - 2) / dims[t]
+        res += fib * (inter * _contraction(n, eo_res and n % 2 == 0)
+                      + (1 - inter) * _contraction(n, False)) * ncells
+    res += nmass * fib * _contraction(n, eo_res and n % 2 == 0) * ncells
+    res += ncells * (16 * d * n ** d + n ** d)
+    if kind in ("acs", "mcs"):
+        m, nsub, fr = n, ncells, [max(0, v - 2) / v for v in dims]
+        eo_ok = eo_fdm and n % 2 == 0
+    else:
+        m = 2 * n
+        nsub = 1
+        for v in dims:
+            nsub *= max(0, v - 1)
+        fr = [max(0, v - 3) / max(1, v - 1) for v in dims]
+        eo_ok = eo_fdm
+    mf = m ** (d - 1)
+    sol = 0.0
+    for t in range(d):
+        per = fr[t] * _contraction(m, eo_ok) + (1 - fr[t]) * _contraction(m, False)
+        sol += 2 * mf * per
+    sol = nsub * (sol + 3 * m ** d)
+    kappa = 1.0
+    if kind == "mvs":
+        kappa = float(2 ** d)
+        for v in dims:
+            kappa *= (v - 1) / v
+    return kappa * res + sol

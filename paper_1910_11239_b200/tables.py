@@ -135,3 +135,95 @@ def build_tables(basis: Basis1D, h: float, dims: tuple[int, ...],
                        beta=-0.5 / h, betap=0.5 / h, cell_z=cz, cell_lam=clam,
                        cell_invsum=cinv, patch_z=pz, patch_lam=plam,
                        patch_invsum=pinv)
+
+
+# ---------------------------------------------------------------------------
+# device packing: even/odd (centro-symmetric) factorisation of the interior
+# digit.  On an interior direction the 1D pencil is symmetric about the cell
+# (patch) midpoint, so the eigenvectors are even or odd and M, A_diag are
+# centro-symmetric: each m x m contraction splits into two (m/2) x (m/2) ones
+# on u = v_i + v_{m-1-i}, w = v_i - v_{m-1-i} (half the FMAs).  The interior
+# eigenpairs are reordered even-first (the FDM inverse is invariant under a
+# consistent permutation of eigenpairs and 1/Lambda-sum).
+# ---------------------------------------------------------------------------
+EO_TOL = 1e-12
+
+
+def _parity(z: np.ndarray):
+    """0/1 parity of each column of z, or None if not exactly symmetric."""
+    par = []
+    scale = np.abs(z).max()
+    for j in range(z.shape[1]):
+        ev = np.abs(z[:, j] - z[::-1, j]).max()
+        od = np.abs(z[:, j] + z[::-1, j]).max()
+        if min(ev, od) > EO_TOL * scale:
+            return None
+        par.append(0 if ev <= od else 1)
+    par = np.array(par)
+    if z.shape[0] % 2 or par.sum() * 2 != z.shape[0]:
+        return None
+    return par
+
+
+def _eo_fdm(z: np.ndarray, lam: np.ndarray):
+    """(permuted z, permuted lam, [fwdE, fwdO, bwdE, bwdO]) or None."""
+    par = _parity(z)
+    if par is None:
+        return None
+    perm = np.concatenate([np.nonzero(par == 0)[0], np.nonzero(par == 1)[0]])
+    zp = z[:, perm]
+    lp = lam[perm]
+    h = z.shape[0] // 2
+    top = zp[:h]
+    halves = np.stack([top[:, :h], top[:, h:], top[:, :h].T, top[:, h:].T])
+    return zp, lp, np.ascontiguousarray(halves)
+
+
+def _cs_halves(a: np.ndarray):
+    """k-outer (transposed) P, Q of a centro-symmetric matrix, or None."""
+    m = a.shape[0]
+    if m % 2 or np.abs(a - a[::-1, ::-1]).max() > EO_TOL * np.abs(a).max():
+        return None
+    h = m // 2
+    p = 0.5 * (a[:h, :h] + a[:h, ::-1][:, :h])
+    q = 0.5 * (a[:h, :h] - a[:h, ::-1][:, :h])
+    return np.stack([p.T, q.T])
+
+
+@dataclass
+class DeviceTables:
+    cell_z: np.ndarray
+    cell_invsum: np.ndarray
+    cell_eo: np.ndarray | None
+    patch_z: np.ndarray | None
+    patch_invsum: np.ndarray | None
+    patch_eo: np.ndarray | None
+    res_eo: np.ndarray | None
+
+
+def device_tables(t: LevelTables, dims: tuple[int, ...], use_eo: bool = True) -> DeviceTables:
+    d = t.dim
+    cz, clam, cinv, ceo = t.cell_z.copy(), t.cell_lam.copy(), t.cell_invsum, None
+    if use_eo:
+        r = _eo_fdm(t.cell_z[0], t.cell_lam[0])
+        if r is not None:
+            cz[0], clam[0], ceo = r
+            cinv = np.zeros_like(t.cell_invsum)
+            for code, digs in _classes(dims, cell_digits):
+                cinv[code] = inverse_sum([clam[dg] for dg in digs]).ravel()
+    pz = pinv = peo = None
+    if t.patch_z is not None:
+        pz, plam, pinv = t.patch_z.copy(), t.patch_lam.copy(), t.patch_invsum
+        if use_eo:
+            r = _eo_fdm(t.patch_z[0], t.patch_lam[0])
+            if r is not None:
+                pz[0], plam[0], peo = r
+                pinv = np.zeros_like(t.patch_invsum)
+                for code, digs in _classes(dims, patch_digits):
+                    pinv[code] = inverse_sum([plam[dg] for dg in digs]).ravel()
+    reo = None
+    if use_eo:
+        mh, ah = _cs_halves(t.mass), _cs_halves(t.adiag[0])
+        if mh is not None and ah is not None:
+            reo = np.ascontiguousarray(np.concatenate([mh, ah]))
+    return DeviceTables(cz, cinv, ceo, pz, pinv, peo, reo)
