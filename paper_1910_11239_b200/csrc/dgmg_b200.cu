@@ -91,10 +91,17 @@ struct FdmArgs {
   int64_t count = 0;
   int packed = 0;
   int atomic = 0;
+  int cluster = 0;  // list holds cluster base vertices (cluster_kernel)
+  int pv_lo = 0, pv_hi = 0;
   const double* invsum = nullptr;
   double omega = 0;
   Geo geo;
 };
+
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
 
 template <typename K>
 static int resident_ctas(K k, int threads, size_t smem, int* out) {
@@ -173,8 +180,36 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
   std::memcpy(p.mats.bwd, hzt, sizeof(p.mats.bwd));
   p.eo = heo != nullptr && M % 2 == 0;
   if (p.eo) std::memcpy(p.mats.eo, heo, sizeof(p.mats.eo));
+  p.pv_lo = q.pv_lo;
+  p.pv_hi = q.pv_hi;
   const int64_t ngroups = (q.count + G - 1) / G;
+  if (!q.atomic && !q.cluster && env_int("DGB_FDM", 2) == 5) {
+    using S5 = Fdm5Shape<D, M, PATCH>;
+    const size_t smem5 = sizeof(double) * S5::SMEM;
+    auto k5 = fdm5_kernel<D, M, PATCH>;
+    static int resident = 0;
+    if (!resident) {
+      DG_CUDA(cudaFuncSetAttribute(k5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
+      if (int rc = resident_ctas(k5, S5::NT, smem5, &resident)) return rc;
+    }
+    k5<<<(unsigned)std::min<int64_t>(ngroups, resident), S5::NT, smem5, st>>>(p, ngroups);
+    DG_CUDA(cudaGetLastError());
+    return DG_OK;
+  }
   const size_t smem = sizeof(double) * fdm2_smem_doubles<D, M>();
+  if constexpr (PATCH) {
+    if (q.cluster) {
+      auto kc = cluster_kernel<D, M>;
+      static bool attr_c = false;
+      if (!attr_c) {
+        DG_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_c = true;
+      }
+      kc<<<(unsigned)ngroups, G * Lay<D, M>::F, smem, st>>>(p);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
+  }
   auto k = fdm2_kernel<D, M, PATCH>;
   static bool attr = false;
   if (!attr) {
@@ -188,11 +223,12 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
 
 struct FlowDev {
   FlowTask* tasks = nullptr;
-  int32_t* item_task = nullptr;
+  int32_t* succ = nullptr;
   int32_t* plist = nullptr;
-  unsigned* ctrl = nullptr;
+  int* state = nullptr;       // live scheduler state
+  int* state_init = nullptr;  // its initial image (copied in before each step)
   int ntasks = 0;
-  int64_t nitems = 0;
+  int64_t units = 0;
 };
 
 template <int D, int N>
@@ -245,12 +281,13 @@ static int launch_flow(const ResArgs& ra, const FdmArgs& fa, const HostRes& h, c
   f.eo = heo != nullptr;
   if (f.eo) std::memcpy(f.mats.eo, heo, sizeof(f.mats.eo));
   p.tasks = fd.tasks;
-  p.item_task = fd.item_task;
+  p.succ = fd.succ;
   p.plist = fd.plist;
-  p.nitems = fd.nitems;
-  p.ctrl = fd.ctrl;
-  DG_CUDA(cudaMemsetAsync(fd.ctrl, 0, sizeof(unsigned) * (1 + fd.ntasks), st));
-  k<<<(unsigned)std::min<int64_t>(fd.nitems, resident), S::NT, smem, st>>>(p);
+  p.state = fd.state;
+  p.ntasks = fd.ntasks;
+  DG_CUDA(cudaMemcpyAsync(fd.state, fd.state_init, sizeof(int) * (4 + 5 * (size_t)fd.ntasks),
+                          cudaMemcpyDeviceToDevice, st));
+  k<<<(unsigned)std::min<int64_t>(fd.units, resident), S::NT, smem, st>>>(p);
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }
@@ -355,6 +392,7 @@ struct dg_level {
   std::vector<DevList> pcol_pk;     // same, packed vertex coordinates
   std::vector<DevList> pcol_cells;  // cells covered by a patch colour (MVS), local ids
   std::vector<DevList> pcol_cells_pk;
+  std::vector<DevList> clus_pk;     // AVS clusters per cluster colour, packed base vertices
   FlowDev flow;                     // dataflow AVS step (flow.cuh)
   bool flow_ok = false;
   cudaStream_t cap = nullptr;       // capture stream
@@ -373,13 +411,15 @@ static int upload_list(const std::vector<int32_t>& h, DevList* out) {
 static void free_level(dg_level* L) {
   if (!L) return;
   for (auto& kv : L->graphs) cudaGraphExecDestroy(kv.second);
-  for (auto* v : {&L->rb, &L->rb_pk, &L->pcol, &L->pcol_pk, &L->pcol_cells, &L->pcol_cells_pk})
+  for (auto* v : {&L->rb, &L->rb_pk, &L->pcol, &L->pcol_pk, &L->pcol_cells, &L->pcol_cells_pk,
+                  &L->clus_pk})
     for (auto& l : *v) cudaFree(l.ptr);
   cudaFree(L->dtab);
   cudaFree(L->flow.tasks);
-  cudaFree(L->flow.item_task);
+  cudaFree(L->flow.succ);
   cudaFree(L->flow.plist);
-  cudaFree(L->flow.ctrl);
+  cudaFree(L->flow.state);
+  cudaFree(L->flow.state_init);
   if (L->cap) cudaStreamDestroy(L->cap);
   delete L;
 }
@@ -431,10 +471,6 @@ static int check_layers(const dg_level* L, int z0, int z1) {
 // dataflow task graph of the AVS step (flow.cuh): z-blocks of `W` vertex
 // layers, colour skew `skew` between consecutive blocks.
 // ---------------------------------------------------------------------------
-static int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e && *e ? std::atoi(e) : dflt;
-}
 
 static int build_flow(dg_level* L) {
   int gp = 0, gr = 0;
@@ -507,6 +543,28 @@ static int build_flow(dg_level* L) {
     if (i < ptasks.size()) seq.push_back(ptasks[i]);
   }
   const int nt = (int)seq.size();
+  // locality edges: block b starts only when block b-1 has finished colour `lag`
+  const int lag = std::max(0, env_int("DGB_FLOW_LAG", 7));
+  std::vector<std::vector<int>> extra(nt);
+  {
+    std::map<std::pair<int, int>, int> pos;  // (blk, colour) -> sequence index
+    for (int j = 0; j < nt; ++j)
+      if (seq[j].type == 1) pos[{seq[j].blk, seq[j].colour}] = j;
+    for (int j = 0; j < nt; ++j) {
+      if (seq[j].type != 1 || seq[j].blk == 0) continue;
+      // first colour of the block (smallest colour present)
+      bool first = true;
+      for (int c = 0; c < seq[j].colour; ++c)
+        if (pos.count({seq[j].blk, c})) first = false;
+      if (!first) continue;
+      int best = -1;  // colour <= lag of the previous block, latest present
+      for (int c = 0; c <= std::min(lag, ncol - 1); ++c) {
+        auto it = pos.find({seq[j].blk - 1, c});
+        if (it != pos.end()) best = it->second;
+      }
+      if (best >= 0 && best < j) extra[j].push_back(best);
+    }
+  }
   // dependencies (conflicting earlier tasks), transitively reduced
   const int words = (nt + 63) / 64;
   std::vector<std::vector<uint64_t>> anc(nt, std::vector<uint64_t>(words, 0));
@@ -517,43 +575,66 @@ static int build_flow(dg_level* L) {
     return a.hi >= b.lo && b.hi >= a.lo;  // R(z) vs P: x/r layer overlap
   };
   for (int j = 0; j < nt; ++j) {
+    auto keep = [&](int i) {
+      seq[j].deps.push_back(i);
+      anc[j][i / 64] |= uint64_t(1) << (i % 64);
+      for (int w = 0; w < words; ++w) anc[j][w] |= anc[i][w];
+    };
+    for (int i : extra[j]) keep(i);
     for (int i = j - 1; i >= 0; --i) {
       if (!conflict(seq[i], seq[j])) continue;
       if (seq[j].type == 0) return fail(DG_EINVAL, "flow: residual after a conflicting patch task");
       if (anc[j][i / 64] >> (i % 64) & 1) continue;  // implied by a kept dependency
-      seq[j].deps.push_back(i);
-      anc[j][i / 64] |= uint64_t(1) << (i % 64);
-      for (int w = 0; w < words; ++w) anc[j][w] |= anc[i][w];
+      keep(i);
     }
-    if ((int)seq[j].deps.size() > FLOW_MAX_DEPS) return DG_OK;  // keep colour launches
   }
+  // device images: tasks with successor lists (CSR), initial scheduler state
+  std::vector<std::vector<int>> succ(nt);
+  for (int j = 0; j < nt; ++j)
+    for (int i : seq[j].deps) succ[i].push_back(j);
   std::vector<FlowTask> ht(nt);
-  std::vector<int32_t> item_task;
+  std::vector<int32_t> sflat;
+  int64_t units = 0;
   for (int j = 0; j < nt; ++j) {
     FlowTask& t = ht[j];
     const int g = seq[j].type == 0 ? gr : gp;
     t.type = seq[j].type;
     t.units = (int)((seq[j].count + g - 1) / g);
-    t.first_item = (int64_t)item_task.size();
     t.start = seq[j].start;
     t.count = seq[j].count;
-    t.ndeps = (int)seq[j].deps.size();
-    for (int i = 0; i < FLOW_MAX_DEPS; ++i) t.deps[i] = i < t.ndeps ? seq[j].deps[i] : -1;
-    if (env_int("DGB_FLOW_NODEPS", 0)) t.ndeps = 0;  // timing experiment only (wrong results)
-    item_task.insert(item_task.end(), t.units, j);
+    t.succ_off = (int)sflat.size();
+    t.nsucc = (int)succ[j].size();
+    sflat.insert(sflat.end(), succ[j].begin(), succ[j].end());
+    units += t.units;
   }
+  std::vector<int> state(4 + 5 * (size_t)nt, 0);
+  int* pend = state.data() + 4;
+  int* queue = pend + 3 * nt;
+  int* valid = queue + nt;
+  int q = 0;
+  for (int j = 0; j < nt; ++j) {
+    pend[j] = (int)seq[j].deps.size();
+    if (pend[j] == 0) {
+      queue[q] = j;
+      valid[q] = 1;
+      ++q;
+    }
+  }
+  state[1] = q;  // tail
   FlowDev& f = L->flow;
   DG_CUDA(cudaMalloc(&f.tasks, sizeof(FlowTask) * nt));
   DG_CUDA(cudaMemcpy(f.tasks, ht.data(), sizeof(FlowTask) * nt, cudaMemcpyHostToDevice));
-  DG_CUDA(cudaMalloc(&f.item_task, sizeof(int32_t) * item_task.size()));
-  DG_CUDA(cudaMemcpy(f.item_task, item_task.data(), sizeof(int32_t) * item_task.size(),
-                     cudaMemcpyHostToDevice));
+  DG_CUDA(cudaMalloc(&f.succ, sizeof(int32_t) * std::max<size_t>(1, sflat.size())));
+  if (!sflat.empty())
+    DG_CUDA(cudaMemcpy(f.succ, sflat.data(), sizeof(int32_t) * sflat.size(), cudaMemcpyHostToDevice));
   DG_CUDA(cudaMalloc(&f.plist, sizeof(int32_t) * std::max<size_t>(1, plist.size())));
   if (!plist.empty())
     DG_CUDA(cudaMemcpy(f.plist, plist.data(), sizeof(int32_t) * plist.size(), cudaMemcpyHostToDevice));
-  DG_CUDA(cudaMalloc(&f.ctrl, sizeof(unsigned) * (1 + nt)));
+  DG_CUDA(cudaMalloc(&f.state, sizeof(int) * state.size()));
+  DG_CUDA(cudaMalloc(&f.state_init, sizeof(int) * state.size()));
+  DG_CUDA(cudaMemcpy(f.state_init, state.data(), sizeof(int) * state.size(), cudaMemcpyHostToDevice));
   f.ntasks = nt;
-  f.nitems = (int64_t)item_task.size();
+  f.units = units;
   L->flow_ok = true;
   return DG_OK;
 }
@@ -740,6 +821,37 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
       if (!rc) rc = upload_list(ccp[k], &bp);
       L->pcol_cells_pk.push_back(bp);
       if (rc) { free_level(L); return rc; }
+    }
+  }
+  // 2^d-patch clusters for the additive step (cluster_kernel): base vertex
+  // v0 = 2a+1 per direction, colour = parity of a; only clusters with a patch
+  // vertex in [pv_begin, pv_end] along the last direction
+  if (L->has_patch) {
+    bool ok = true;
+    for (int t = 0; t < d; ++t) ok = ok && nc[t] >= 2;
+    const int vlo = std::max(1, desc->pv_begin), vhi = std::min(nc[d - 1] - 1, desc->pv_end);
+    if (ok && vlo <= vhi) {
+      const int ncl = 1 << d;
+      std::vector<std::vector<int32_t>> cl(ncl);
+      int na[3] = {1, 1, 1};
+      for (int t = 0; t < d; ++t) na[t] = nc[t] / 2;  // a = 0 .. (nc-2)/2 covers v = 1 .. nc-1
+      int a[3] = {0, 0, 0};
+      for (a[2] = 0; a[2] < (d == 3 ? na[2] : 1); ++a[2])
+        for (a[1] = 0; a[1] < na[1]; ++a[1])
+          for (a[0] = 0; a[0] < na[0]; ++a[0]) {
+            const int zlo = 2 * a[d - 1] + 1, zhi = 2 * a[d - 1] + 2;
+            if (zhi < vlo || zlo > vhi) continue;
+            int col = 0;
+            for (int t = 0; t < d; ++t) col |= (a[t] & 1) << t;
+            cl[col].push_back(pack3(2 * a[0] + 1, 2 * a[1] + 1, d == 3 ? 2 * a[2] + 1 : 0));
+          }
+      for (int k = 0; k < ncl; ++k) {
+        if (cl[k].empty()) continue;
+        DevList dl;
+        int rc = upload_list(cl[k], &dl);
+        L->clus_pk.push_back(dl);
+        if (rc) { free_level(L); return rc; }
+      }
     }
   }
   if (desc->own_begin < zb || desc->own_end > zb + desc->z_count ||
@@ -931,6 +1043,21 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
                              L->peo(), L->flow, st);
       }
       if ((rc = res_range())) return rc;
+      if (env_int("DGB_CLUSTER", 0) && !L->clus_pk.empty()) {
+        for (auto& c : L->clus_pk) {
+          ++*nl;
+          FdmArgs p = fdm_params(L, true, r, x, omega);
+          p.list = c.ptr;
+          p.count = c.count;
+          p.packed = 1;
+          p.cluster = 1;
+          p.pv_lo = std::max(1, L->desc.pv_begin);
+          p.pv_hi = std::min(L->desc.ncells[L->d - 1] - 1, L->desc.pv_end);
+          if ((rc = dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), L->peo(), st)))
+            return rc;
+        }
+        return DG_OK;
+      }
       for (auto& c : L->pcol_pk) {
         ++*nl;
         if ((rc = patch_fdm_packed(L, r, x, omega, c, st))) return rc;

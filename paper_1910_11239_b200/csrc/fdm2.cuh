@@ -45,6 +45,7 @@ struct Fdm2Params {
   int atomic;   // overlapping subdomains: fp64 reductions instead of load-add-store
   int packed;   // list entries are packed global coordinates (pack3)
   int eo;       // interior digit uses the even/odd halves
+  int pv_lo, pv_hi;  // cluster mode: patch vertices v_d outside are skipped
   Geo geo;
   FdmMats<M> mats;
 };
@@ -338,7 +339,7 @@ struct Rows {
 template <int D, int M, bool PATCH, int G>
 __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32_t* list,
                                           int packed, int64_t start, int64_t count, int64_t grp,
-                                          double* sm, bool coherent) {
+                                          double* sm, bool coherent, int delta = -1) {
   using L = Lay<D, M>;
   using R = Rows<D, M, PATCH>;
   constexpr int N = R::N;
@@ -354,8 +355,21 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     inf[7] = idx < count;
     int digit[3] = {0, 0, 0}, base[3] = {0, 0, 0};
     if (inf[7]) {
-      const int id = list ? list[idx] : (int)(start + idx);
-      subdomain_info<D, PATCH>(p.geo, id, packed != 0, digit, base);
+      int id = list ? list[idx] : (int)(start + idx);
+      if (PATCH && delta >= 0) {
+        // cluster mode: list holds packed base vertices of 2^d-patch clusters
+        int v[3] = {id & 1023, (id >> 10) & 1023, (id >> 20) & 1023};
+        bool ok = true;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+          v[t] += (delta >> t) & 1;
+          ok = ok && v[t] >= 1 && v[t] <= p.geo.nc[t] - 1;
+        }
+        ok = ok && v[D - 1] >= p.pv_lo && v[D - 1] <= p.pv_hi;
+        inf[7] = ok;
+        id = pack3(v[0], v[1], D == 3 ? v[2] : 0);
+      }
+      if (inf[7]) subdomain_info<D, PATCH>(p.geo, id, packed != 0, digit, base);
     }
     int cls = 0;
 #pragma unroll
@@ -434,6 +448,187 @@ fdm2_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
                                               sm, false);
 }
 
+
+
+// ---------------------------------------------------------------------------
+// fdm5: persistent, software-pipelined solves.  Each CTA walks its groups of
+// G subdomains; cp.async brings the r rows of the next group into the second
+// (padded) tensor buffer and the x rows of the current group into an
+// unpadded buffer while the current group is contracted, so neither the
+// gather of r nor the load half of the x update is exposed.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(double* sdst, const double* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
+template <int D, int M, bool PATCH>
+struct Fdm5Shape {
+  using R = Rows<D, M, PATCH>;
+  static constexpr int N = R::N;
+  static constexpr int NEc = (D == 3) ? N * N * N : N * N;
+  static constexpr int G = fdm2_groups<D, M>();
+  static constexpr int NT = G * Lay<D, M>::F;
+  static constexpr int SZ = Lay<D, M>::SZ;
+  static constexpr int XSZ = R::SLOTS * NEc;
+  static constexpr int SMEM = 2 * G * SZ + G * XSZ;  // doubles
+};
+
+template <int D, int M, bool PATCH>
+__global__ void __launch_bounds__(Fdm5Shape<D, M, PATCH>::NT)
+fdm5_kernel(const __grid_constant__ Fdm2Params<D, M> p, int64_t ngroups) {
+  using L = Lay<D, M>;
+  using R = Rows<D, M, PATCH>;
+  using S = Fdm5Shape<D, M, PATCH>;
+  constexpr int N = S::N, G = S::G, F = L::F, NT = S::NT;
+  extern __shared__ double sm[];
+  double* Xs = sm + 2 * G * S::SZ;
+  __shared__ int s_info[2][G][8];            // digit[3], cls, active
+  __shared__ int64_t s_cell[2][G][R::SLOTS];  // dof offset of each cell
+  const int tid = threadIdx.x;
+  const int g = tid / F, f = tid - (tid / F) * F;
+
+  auto info = [&](int64_t grp, int st) {
+    if (tid < G) {
+      const int64_t idx = grp * G + tid;
+      int* inf = s_info[st][tid];
+      inf[7] = idx < p.count;
+      int digit[3] = {0, 0, 0}, base[3] = {0, 0, 0};
+      if (inf[7]) {
+        const int id = p.list ? p.list[idx] : (int)(p.start + idx);
+        subdomain_info<D, PATCH>(p.geo, id, p.packed != 0, digit, base);
+      }
+      int cls = 0;
+#pragma unroll
+      for (int t = D - 1; t >= 0; --t) cls = cls * 4 + digit[t];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) inf[t] = digit[t];
+      inf[6] = cls;
+#pragma unroll
+      for (int s = 0; s < R::SLOTS; ++s) {
+        int c[3] = {base[0] + (s & 1), base[1] + ((s >> 1) & 1), base[2] + ((s >> 2) & 1)};
+        if (!PATCH) c[0] = base[0], c[1] = base[1], c[2] = base[2];
+        s_cell[st][tid][s] = (int64_t)cell_local<D>(p.geo, c) * S::NEc;
+      }
+    }
+  };
+  auto issue_r = [&](int st) {
+    double* base = sm + st * G * S::SZ;
+    for (int row = tid; row < G * R::RPS; row += NT) {
+      const int gg = row / R::RPS;
+      if (!s_info[st][gg][7]) continue;
+      int slot, goff, soff;
+      R::map(row - gg * R::RPS, slot, goff, soff);
+      const double* src = p.r + s_cell[st][gg][slot] + goff;
+      double* dst = base + gg * S::SZ + soff;
+#pragma unroll
+      for (int i = 0; i < N; ++i) cp_async8(dst + i, src + i);
+    }
+    cp_async_commit();
+  };
+  auto issue_x = [&](int st) {
+    for (int row = tid; row < G * R::RPS; row += NT) {
+      const int gg = row / R::RPS;
+      if (!s_info[st][gg][7]) continue;
+      const int rr = row - gg * R::RPS;
+      const int slot = rr / R::RPC, w = rr - slot * R::RPC;
+      const double* src = p.x + s_cell[st][gg][slot] + w * N;
+      double* dst = Xs + gg * S::XSZ + slot * S::NEc + w * N;
+      if constexpr (N % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < N; i += 2) cp_async16(dst + i, src + i);
+      } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) cp_async8(dst + i, src + i);
+      }
+    }
+    cp_async_commit();
+  };
+
+  int64_t grp = blockIdx.x;
+  if (grp >= ngroups) return;
+  info(grp, 0);
+  __syncthreads();
+  issue_r(0);
+  for (int st = 0; grp < ngroups; grp += gridDim.x, st ^= 1) {
+    issue_x(st);
+    const int64_t nxt = grp + gridDim.x;
+    const bool more = nxt < ngroups;
+    if (more) {
+      info(nxt, st ^ 1);
+      __syncthreads();
+      issue_r(st ^ 1);
+      cp_async_wait<2>();  // r of this group landed (x of it and r of the next may fly)
+    } else {
+      cp_async_wait<1>();
+    }
+    __syncthreads();
+    const int* dg = s_info[st][g];
+    const bool active = dg[7];
+    double* buf = sm + (st * G + g) * S::SZ;
+#pragma unroll
+    for (int t = 0; t < D - 1; ++t) {
+      if (active) fdm_fiber<M, true>(p.mats, p.eo, dg[t], buf, L::sbase(t, f), L::sstride(t));
+      __syncthreads();
+    }
+    if (active) {
+      constexpr int t = D - 1;
+      const int sb = L::sbase(t, f), ss = L::sstride(t);
+      const double* inv = p.invsum + (int64_t)dg[6] * L::NE + L::gbase(t, f);
+      double v[M], o[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) v[k] = buf[sb + k * ss];
+      fdm_matvec<M, true>(p.mats, p.eo, dg[t], v, o);
+#pragma unroll
+      for (int k = 0; k < M; ++k) o[k] *= __ldg(inv + k * L::gstride(t));
+      fdm_matvec<M, false>(p.mats, p.eo, dg[t], o, v);
+#pragma unroll
+      for (int k = 0; k < M; ++k) buf[sb + k * ss] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < D - 1; ++s) {
+      const int t = D - 2 - s;
+      if (active) fdm_fiber<M, false>(p.mats, p.eo, dg[t], buf, L::sbase(t, f), L::sstride(t));
+      __syncthreads();
+    }
+    if (more) cp_async_wait<1>();  // x of this group landed
+    else cp_async_wait<0>();
+    __syncthreads();
+    double* rb = sm + st * G * S::SZ;
+    for (int row = tid; row < G * R::RPS; row += NT) {
+      const int gg = row / R::RPS;
+      if (!s_info[st][gg][7]) continue;
+      int slot, goff, soff;
+      R::map(row - gg * R::RPS, slot, goff, soff);
+      const double* y = rb + gg * S::SZ + soff;
+      const double* xs = Xs + gg * S::XSZ + slot * S::NEc + goff;
+      double v[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[i] = fma(p.omega, y[i], xs[i]);
+      row_store<N>(p.x + s_cell[st][gg][slot] + goff, v);
+    }
+    __syncthreads();  // X and this stage's buffers are refilled next
+  }
+}
+
+// Additive patch step over 2^d-patch clusters (vertices {2a+1, 2a+2}^d): one
+// group of threads owns a cluster and solves its patches one after another,
+// so the cluster's 3^d cells of r and x stay in L1/L2 across the 2^d solves
+// (~3^d/8 cell loads per patch instead of 2^d).  Clusters of one launch share
+// the parity of a (2^d launches per step): they are 2 cells apart, so their
+// writes are disjoint and no atomics are needed.
+template <int D, int M>
+__global__ void __launch_bounds__(fdm2_groups<D, M>() * Lay<D, M>::F)
+cluster_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
+  extern __shared__ double sm[];
+#pragma unroll 1
+  for (int delta = 0; delta < (1 << D); ++delta) {
+    fdm_group<D, M, true, fdm2_groups<D, M>()>(p, p.list, 1, 0, p.count, blockIdx.x, sm, false,
+                                               delta);
+    __syncthreads();  // the next patch of each cluster overlaps this one
+  }
+}
 
 template <int D, int M>
 __host__ __device__ constexpr int fdm2_smem_doubles() {

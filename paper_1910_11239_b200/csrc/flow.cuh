@@ -1,40 +1,46 @@
 // flow.cuh - the whole additive vertex-patch smoothing step (AVS) as one
-// persistent, dependency-driven ("dataflow") kernel.
+// persistent, dependency-driven ("dataflow") kernel with a ready queue.
 //
 // Colour-by-colour launches stream the whole level through HBM once per
-// colour (16 x ~0.6 GB at cfg 5) because a colour touches every z-layer.  Here
-// the step is cut into tasks:
+// colour (16 x ~0.6 GB at cfg 5) because every colour touches every z-layer.
+// Here the step is cut into tasks
 //   R(z)    residual r = b - A x on cell layer z            (res_group)
 //   P(b, c) patches of colour c whose vertex layer lies in z-block b (fdm_group)
-// sequenced so that a few neighbouring z-blocks are in flight at any time
-// (colour skew between consecutive blocks), which keeps their cells resident
-// in the 126 MB L2.  Every task carries the list of earlier tasks it conflicts
-// with (built on the host, transitively reduced):
-//   - P after P: different colours touching a common cell layer (the
-//     reference's colour order per DoF is preserved: ascending colours);
-//   - P after R: the patch reads r of, or writes x read by, the residual.
-// CTAs claim work items (task, unit) in sequence order from a global counter,
-// wait (acquire loads) until the dependencies have completed all their units,
-// run the unit, and publish completion (fence + atomic add).  An item only
-// waits on items earlier in the sequence, all claimed by running CTAs, so the
-// schedule cannot deadlock.  Per DoF the additions happen in the same order as
-// in the colour-by-colour launches, so the result is bit-identical to them.
+// with dependencies built on the host (transitively reduced):
+//   - P after P: different colours touching a common cell layer (every DoF
+//     keeps the reference's ascending colour order, so the result is
+//     bit-identical to the colour launches);
+//   - P after R: the patch reads r of, or writes x read by, the residual;
+//   - locality edges P(b, 0) <- P(b-1, lag): block b starts its colours only
+//     when block b-1 is `lag` colours in, so only a few z-blocks (and their
+//     cells) are live at a time and stay resident in the 126 MB L2.
+// Scheduling is push-based: a task whose last unit completes decrements the
+// pending counts of its successors and appends every newly ready one to a
+// global FIFO.  CTAs claim units of the task at the queue head (atomic claim
+// counters), so no CTA ever waits on a specific task -- an idle CTA only polls
+// the queue -- and the schedule cannot deadlock.
 #pragma once
 #include "fdm2.cuh"
 #include "res2.cuh"
 
 namespace dgb {
 
-constexpr int FLOW_MAX_DEPS = 12;
-
 struct FlowTask {
-  int type;            // 0 = residual layer, 1 = patch block x colour
-  int units;           // work units (groups of cells / patches)
-  int64_t first_item;  // index of the task's first work item
-  int64_t start;       // residual: first local cell; patch: offset into plist
-  int64_t count;       // cells / patches
-  int ndeps;
-  int deps[FLOW_MAX_DEPS];
+  int type;       // 0 = residual layer, 1 = patch block x colour
+  int units;      // work units (groups of cells / patches)
+  int64_t start;  // residual: first local cell; patch: offset into plist
+  int64_t count;  // cells / patches
+  int succ_off;   // successors: succ[succ_off .. succ_off + nsucc)
+  int nsucc;
+};
+
+// per-launch scheduler state (reset from a host-built image before each step)
+struct FlowState {
+  int head;       // queue head (first entry that may still have units)
+  int tail;       // queue entries allocated
+  int finished;   // completed tasks
+  int pad;
+  // followed by: pending[nt], claimed[nt], done[nt], queue[nt], valid[nt]
 };
 
 template <int D, int N>
@@ -42,10 +48,10 @@ struct FlowParams {
   Res2Params<D, N> res;
   Fdm2Params<D, 2 * N> fdm;
   const FlowTask* tasks;
-  const int32_t* item_task;
+  const int32_t* succ;
   const int32_t* plist;  // packed patch vertex coordinates, concatenated per task
-  int64_t nitems;
-  unsigned* ctrl;        // [0] next item, [1 + t] completed units of task t
+  int* state;            // FlowState + 5 * ntasks ints
+  int ntasks;
 };
 
 template <int D, int N>
@@ -58,14 +64,17 @@ struct FlowShape {
   static constexpr int SMEM_P = GP * Lay<D, M>::SZ;
   static constexpr int SMEM = SMEM_R > SMEM_P ? SMEM_R : SMEM_P;
   // keep the merged residual + patch code at the register budget of the
-  // standalone kernels (~64 regs) so that 3 CTAs share an SM
+  // standalone kernels so that 3-4 CTAs share an SM
   static constexpr int MIN_CTAS = NT <= 256 ? 4 : 3;
 };
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ int ld_acquire_i(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void st_release_i(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 template <int D, int N>
@@ -73,33 +82,64 @@ __global__ void __launch_bounds__(FlowShape<D, N>::NT, FlowShape<D, N>::MIN_CTAS
 flow_kernel(const __grid_constant__ FlowParams<D, N> p) {
   using S = FlowShape<D, N>;
   extern __shared__ double sm[];
-  __shared__ int64_t s_item;
+  __shared__ int s_task, s_unit;
+  const int nt = p.ntasks;
+  int* st = p.state;
+  int* pending = st + 4;
+  int* claimed = pending + nt;
+  int* done = claimed + nt;
+  int* queue = done + nt;
+  int* valid = queue + nt;
   for (;;) {
-    if (threadIdx.x == 0) s_item = (int64_t)atomicAdd(p.ctrl, 1u);
-    __syncthreads();
-    const int64_t item = s_item;
-    if (item >= p.nitems) break;
-    const int t = p.item_task[item];
-    const FlowTask* T = p.tasks + t;
     if (threadIdx.x == 0) {
-      const int nd = T->ndeps;
-      for (int i = 0; i < nd; ++i) {
-        const int dd = T->deps[i];
-        const unsigned need = (unsigned)p.tasks[dd].units;
-        while (ld_acquire(p.ctrl + 1 + dd) < need) __nanosleep(64);
+      int task = -1, unit = 0;
+      for (;;) {
+        const int h = ld_acquire_i(st + 0);
+        if (h < ld_acquire_i(st + 1)) {
+          while (!ld_acquire_i(valid + h)) __nanosleep(32);
+          const int t = queue[h];
+          const int u = atomicAdd(claimed + t, 1);
+          if (u < p.tasks[t].units) {
+            task = t;
+            unit = u;
+            break;
+          }
+          atomicCAS(st + 0, h, h + 1);  // head task fully claimed: advance
+          continue;
+        }
+        if (ld_acquire_i(st + 2) >= nt) break;  // everything done
+        __nanosleep(128);
       }
+      s_task = task;
+      s_unit = unit;
     }
     __syncthreads();
-    const int64_t unit = item - T->first_item;
-    if (T->type == 0) {
-      res_group<D, N, S::GR>(p.res, nullptr, 0, T->start, T->count, unit, sm);
+    const int t = s_task;
+    const int unit = s_unit;
+    if (t < 0) break;
+    const FlowTask T = p.tasks[t];
+    if (T.type == 0) {
+      res_group<D, N, S::GR>(p.res, nullptr, 0, T.start, T.count, unit, sm);
     } else {
-      fdm_group<D, S::M, true, S::GP>(p.fdm, p.plist + T->start, 1, 0, T->count, unit, sm, true);
+      fdm_group<D, S::M, true, S::GP>(p.fdm, p.plist + T.start, 1, 0, T.count, unit, sm, true);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      atomicAdd(p.ctrl + 1 + t, 1u);
+      if (atomicAdd(done + t, 1) == T.units - 1) {  // last unit of the task
+        __threadfence();
+        for (int i = 0; i < T.nsucc; ++i) {
+          const int s = p.succ[T.succ_off + i];
+          if (atomicSub(pending + s, 1) == 1) {  // successor became ready
+            const int pos = atomicAdd(st + 1, 1);
+            queue[pos] = s;
+            __threadfence();
+            st_release_i(valid + pos, 1);
+          }
+        }
+        __threadfence();
+        atomicAdd(st + 2, 1);
+      }
     }
   }
 }

@@ -264,6 +264,7 @@ def test_dataflow_avs_kernel_bitwise_equals_colour_launches(d, nc, k, monkeypatc
     work across z-blocks but keeps every DoF's colour order: bit-identical."""
     ctx, _, sm = _setup(d, nc, k, "avs", 0.25)
     x0, b = inputs(ctx.ndofs, 6)
+    monkeypatch.setenv("DGB_CLUSTER", "0")
     monkeypatch.setenv("DGB_FLOW", "0")
     xa = x0.copy()
     sm.smooth(xa, b)
@@ -273,5 +274,23 @@ def test_dataflow_avs_kernel_bitwise_equals_colour_launches(d, nc, k, monkeypatc
     sm.use_graph = False
     sm.smooth(xb, b)
     assert np.array_equal(xa, xb)
+    want = OracleLevel((nc,) * d, k).smooth("avs", 0.25, x0, b)
+    assert rel(xb, want) <= RTOL
+
+
+@pytest.mark.parametrize("d,nc,k", [(3, 12, 3), (3, 9, 5), (2, 21, 4), (3, 7, 7), (3, 2, 2)])
+def test_cluster_avs_matches_colour_launches_and_oracle(d, nc, k, monkeypatch):
+    """The default additive patch path solves 2^d-patch clusters per launch
+    (cluster_kernel): same update, different summation order per DoF."""
+    ctx, _, sm = _setup(d, nc, k, "avs", 0.25)
+    x0, b = inputs(ctx.ndofs, 8)
+    monkeypatch.setenv("DGB_CLUSTER", "0")
+    xa = x0.copy()
+    sm.use_graph = False
+    sm.smooth(xa, b)
+    monkeypatch.setenv("DGB_CLUSTER", "1")
+    xb = x0.copy()
+    sm.smooth(xb, b)
+    assert rel(xb - x0, xa - x0) <= 1e-13
     want = OracleLevel((nc,) * d, k).smooth("avs", 0.25, x0, b)
     assert rel(xb, want) <= RTOL
