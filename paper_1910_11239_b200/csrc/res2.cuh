@@ -190,51 +190,45 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
     mass_fiber<D, N, false>(p, 0, f, B, nullptr);
   }
   __syncthreads();
+  // each thread's last fiber (t = 0) is exactly cell row f, so the final
+  // contraction writes r = b - A x straight to global memory; b is
+  // prefetched into registers one phase earlier
+  const int64_t gi = (int64_t)(active ? cell : 0) * L::NE + f * N;
+  double bv[N];
   if (D == 3) {
     if (active) {
       mass_fiber<D, N, true>(p, 2, f, A, B);   // A = M_2 (M_1 G_0 + M_0 G_1)
       stiff2_fiber<D, N>(p, 2, f, c, X, B);    // B = G_2 (same fibers as above)
     }
     __syncthreads();
+    if (active && p.b) row_load_reg<N>(bv, p.b + gi);
     if (active) mass_fiber<D, N, false>(p, 1, f, B, nullptr);
     __syncthreads();
-    if (active) {  // A += M_0 B
+    if (active) {  // r = b - (A + M_0 B), row f
       const int sb = L::sbase(0, f);
       double v[N], o[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) v[k] = B[sb + k];
       res_mass<D, N>(p, v, o);
 #pragma unroll
-      for (int k = 0; k < N; ++k) A[sb + k] += o[k];
+      for (int k = 0; k < N; ++k) {
+        const double ax = A[sb + k] + o[k];
+        o[k] = p.b ? bv[k] - ax : ax;
+      }
+      row_store<N>(p.r + gi, o);
     }
   } else {
-    // 2D: OUT = M_1 G_0 + M_0 G_1 = A + B
+    if (active && p.b) row_load_reg<N>(bv, p.b + gi);
+    // 2D: A x = M_1 G_0 + M_0 G_1 = A + B, row f
     if (active) {
       const int sb = L::sbase(0, f);
+      double o[N];
 #pragma unroll
-      for (int k = 0; k < N; ++k) A[sb + k] += B[sb + k];
-    }
-  }
-  __syncthreads();
-  for (int row = tid; row < G * R::RPS; row += NT) {
-    const int gg = row / R::RPS;
-    const int cl = s_cell[gg];
-    if (cl < 0) continue;
-    int slot, goff, soff;
-    R::map(row - gg * R::RPS, slot, goff, soff);
-    const int64_t gi = (int64_t)cl * L::NE + goff;
-    const double* a = sm + (G + gg) * L::SZ + soff;
-    if (p.b) {
-      double bv[N];
-      row_load_reg<N>(bv, p.b + gi);
-#pragma unroll
-      for (int i = 0; i < N; ++i) bv[i] -= a[i];
-      row_store<N>(p.r + gi, bv);
-    } else {
-      double av[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) av[i] = a[i];
-      row_store<N>(p.r + gi, av);
+      for (int k = 0; k < N; ++k) {
+        const double ax = A[sb + k] + B[sb + k];
+        o[k] = p.b ? bv[k] - ax : ax;
+      }
+      row_store<N>(p.r + gi, o);
     }
   }
 }
