@@ -208,14 +208,21 @@ def run_ours(args, cfg):
     if args.gpus != ws and ws > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
     torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    slab = ws > 1 or args.slab
+    if slab:
+        if not dist.is_initialized():
+            if ws == 1:
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29531")
+                os.environ.setdefault("RANK", "0")
+                os.environ.setdefault("WORLD_SIZE", "1")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     d, nc, k, kind, omega = cfg["d"], cfg["nc"], cfg["k"], cfg["kind"], cfg["omega"]
-    if ws > 1 and args.config != 5:
-        raise SystemExit("multi-GPU runs use the cfg-5 weak-scaling workload")
-    dims = (nc,) * d if ws == 1 else (nc, nc, nc * ws)
+    if slab and args.config != 5:
+        raise SystemExit("multi-GPU (slab) runs use the cfg-5 weak-scaling workload")
+    dims = (nc,) * d if not slab else (nc, nc, nc * ws)
 
-    if ws == 1:
+    if not slab:
         lvl = dg.build_hierarchy(d, nc, 0).levels[0]
         basis = dg.Basis1D.make(k)
         ctx = dg.make_context(lvl, basis, 1.0)
@@ -228,15 +235,15 @@ def run_ours(args, cfg):
         n_local = step_obj.n_owned
     n_global = n_local * ws
 
-    # seeded inputs, generated on the host once (rank-local slab of the global vectors)
-    rng_off = rank * n_local
-    b_h = np.random.default_rng(0).uniform(-1.0, 1.0, n_global)[rng_off:rng_off + n_local] \
-        if ws > 1 else np.random.default_rng(0).uniform(-1.0, 1.0, n_local)
-    x_h = np.random.default_rng(1).uniform(-1.0, 1.0, n_global)[rng_off:rng_off + n_local] \
-        if ws > 1 else np.random.default_rng(1).uniform(-1.0, 1.0, n_local)
+    # seeded inputs generated on the host: seeds 0 / 1 on one GPU (the tests'
+    # and the oracle's inputs); per-rank streams [0, rank] / [1, rank] on N > 1
+    # (each rank only materialises its own slab)
+    s_b, s_x = (0, 1) if ws == 1 else ([0, rank], [1, rank])
+    b_h = np.random.default_rng(s_b).uniform(-1.0, 1.0, n_local)
+    x_h = np.random.default_rng(s_x).uniform(-1.0, 1.0, n_local)
     stream = torch.cuda.current_stream()
 
-    if ws == 1:
+    if not slab:
         x = torch.from_numpy(x_h).cuda()
         b = torch.from_numpy(b_h).cuda()
 
@@ -249,7 +256,7 @@ def run_ours(args, cfg):
             step_obj.step()
 
     def barrier():
-        if ws > 1:
+        if slab:
             dist.barrier()
 
     for _ in range(args.warmup):
@@ -270,7 +277,7 @@ def run_ours(args, cfg):
     barrier()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
-    if ws > 1:
+    if slab:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -279,9 +286,10 @@ def run_ours(args, cfg):
 
     # ---- per-kernel split (dominant kernel for the roofline), direct launches
     kt = step_obj.kernel_times(reps=max(3, min(args.steps, 10)))
-    flops_step, bytes_step = F.step_work(kind, d, k, dims if ws == 1 else (nc, nc, nc))
+    rdims = dims if not slab else (nc, nc, nc)  # per-GPU share of the work
+    flops_step, bytes_step = F.step_work(kind, d, k, rdims)
     if kind in ("avs", "mvs"):
-        npatch = int(np.prod([v - 1 for v in (dims if ws == 1 else (nc, nc, nc))]))
+        npatch = int(np.prod([v - 1 for v in rdims]))
         f_solve = F.solve_flops(d, 2 * (k + 1), npatch)
         dom = f"fdm2_kernel<{d},{2 * (k + 1)},patch> (all colours)"
     else:
@@ -302,11 +310,10 @@ def run_ours(args, cfg):
     achieved = dom_f / (dom_ms * 1e-3) / 1e12
     # the kernels split interior-digit contractions even/odd (half the FMAs):
     # also report the fraction against the flops actually executed
-    dev = step_obj.ctx.dev if ws == 1 else step_obj._dev
+    dev = step_obj.ctx.dev if not slab else step_obj._dev
     eo = getattr(dev, "eo", {"cell": False, "patch": False, "residual": False})
     eo_fdm = eo["cell"] if kind in ("acs", "mcs") else eo["patch"]
-    fx_step = F.executed_step_flops(kind, d, k, dims if ws == 1 else (nc, nc, nc), eo_fdm,
-                                    eo["residual"])
+    fx_step = F.executed_step_flops(kind, d, k, rdims, eo_fdm, eo["residual"])
     dom_fx = dom_f * fx_step / flops_step
     traffic = None
     try:
@@ -317,7 +324,7 @@ def run_ours(args, cfg):
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
-    if ws == 1:
+    if not slab:
         xh = torch.from_numpy(x_h.copy()).pin_memory()
         bh = torch.from_numpy(b_h.copy()).pin_memory()
         xd = torch.empty_like(xh, device="cuda")
@@ -362,7 +369,7 @@ def run_ours(args, cfg):
             "data": "synthetic (seeded uniform[-1,1] b, x0)",
             "config": {"workload": cfg["name"], "dims": list(dims), "k": k, "kind": kind,
                        "omega": omega, "global_dofs": n_global,
-                       "parallelism": f"slab{ws}" if ws > 1 else "single",
+                       "parallelism": f"slab{ws}" if slab else "single",
                        "l2": "inputs larger than L2 (no flush)" if n_local * 8 > 126e6
                        else "inputs smaller than L2"},
             "roofline": {"bound": "tensor", "pipe": "fp64 (DFMA/DMMA)", "kernel": dom,
@@ -383,7 +390,7 @@ def run_ours(args, cfg):
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if slab:
         dist.destroy_process_group()
 
 
@@ -395,6 +402,8 @@ def main():
     ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--slab", action="store_true",
+                    help="run the multi-GPU slab code path even on one GPU (validation)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

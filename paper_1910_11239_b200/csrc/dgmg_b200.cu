@@ -393,6 +393,7 @@ struct dg_level {
   std::vector<DevList> pcol_cells;  // cells covered by a patch colour (MVS), local ids
   std::vector<DevList> pcol_cells_pk;
   std::vector<DevList> clus_pk;     // AVS clusters per cluster colour, packed base vertices
+  DevList pall_pk;                  // all patches (colour order), packed, one-launch AVS
   FlowDev flow;                     // dataflow AVS step (flow.cuh)
   bool flow_ok = false;
   cudaStream_t cap = nullptr;       // capture stream
@@ -414,6 +415,7 @@ static void free_level(dg_level* L) {
   for (auto* v : {&L->rb, &L->rb_pk, &L->pcol, &L->pcol_pk, &L->pcol_cells, &L->pcol_cells_pk,
                   &L->clus_pk})
     for (auto& l : *v) cudaFree(l.ptr);
+  cudaFree(L->pall_pk.ptr);
   cudaFree(L->dtab);
   cudaFree(L->flow.tasks);
   cudaFree(L->flow.succ);
@@ -809,6 +811,11 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
         }
       }
     }
+    {
+      std::vector<int32_t> all;
+      for (int k = 0; k < ncol; ++k) all.insert(all.end(), pcp[k].begin(), pcp[k].end());
+      if (int rc = upload_list(all, &L->pall_pk)) { free_level(L); return rc; }
+    }
     for (int k = 0; k < ncol; ++k) {
       if (pc[k].empty()) continue;
       DevList a, b, ap, bp;
@@ -1043,6 +1050,22 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
                              L->peo(), L->flow, st);
       }
       if ((rc = res_range())) return rc;
+      // small levels are launch-bound with 16 colour launches: one launch over
+      // all patches with fp64 reductions for the overlaps is faster there
+      // (cfg 2: 0.173 -> 0.145 ms); large levels keep the write-disjoint
+      // colour launches (L2 reduction throughput, cfg 5: 3.37 vs 3.83 ms)
+      const int64_t pdofs = L->pall_pk.count * (L->d == 3 ? (int64_t)L->m * L->m * L->m
+                                                          : (int64_t)L->m * L->m);
+      const int64_t amax = (int64_t)env_int("DGB_AVS_ATOMIC_MAX_MDOFS", 64) * 1000000;
+      if (env_int("DGB_AVS_ATOMIC", 1) && L->pall_pk.count > 0 && pdofs <= amax) {
+        ++*nl;
+        FdmArgs p = fdm_params(L, true, r, x, omega);
+        p.list = L->pall_pk.ptr;
+        p.count = L->pall_pk.count;
+        p.packed = 1;
+        p.atomic = 1;
+        return dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), L->peo(), st);
+      }
       if (env_int("DGB_CLUSTER", 0) && !L->clus_pk.empty()) {
         for (auto& c : L->clus_pk) {
           ++*nl;

@@ -31,6 +31,7 @@ from .tables import SingularLocalSolverError, cell_digits, patch_digits
 
 __all__ = [
     "LocalSolver",
+    "apply_inverse",
     "EigenPair1D",
     "SingularLocalSolverError",
     "CellSolverSet",
@@ -57,10 +58,50 @@ class LocalSolver:
     sizes: tuple
     eigenpairs: list
     inv_sum_rev: np.ndarray
+    _set: object = None        # owning solver set (device execution)
+    _rep: int = -1             # representative subdomain id of the class
 
     @property
     def ndofs(self) -> int:
         return int(np.prod(self.sizes))
+
+    def apply_inverse(self, r):
+        return apply_inverse(self, r)
+
+
+def apply_inverse(solver: LocalSolver, r):
+    """x = Z diag(1/sum lam) Z^T r for one subdomain (`fastdiag.py:122-133`),
+    run by the level's FDM kernel on a representative subdomain of the class:
+    r is placed on that subdomain's dofs of a zero level vector, solved with
+    omega = 1 into a zero x, and read back through the same index map."""
+    if np.asarray(r).size != solver.ndofs:
+        raise ValueError("residual size does not match subdomain")
+    sset = solver._set
+    if sset is None:
+        raise ValueError("LocalSolver is not attached to a device solver set")
+    ctx = sset.ctx
+    dev = ctx.dev
+    n = ctx.ndofs
+    shape = np.shape(r)
+    rr = np.asarray(r, dtype=np.float64).reshape(-1)
+    j = solver._rep
+    if sset.kind == "cell":
+        nd = sset.cell_dofs
+        idx = torch.arange(j * nd, (j + 1) * nd, device="cuda")
+    else:
+        idx = torch.from_numpy(sset.gather_map(np.array([j]))[0]).cuda()
+    rv = torch.zeros(n, dtype=torch.float64, device="cuda")
+    xv = torch.zeros(n, dtype=torch.float64, device="cuda")
+    rv[idx] = torch.from_numpy(rr).cuda()
+    ids = torch.tensor([j], dtype=torch.int32, device="cuda")
+    if sset.kind == "cell":
+        _lib.check(dev._lib.dg_cell_fdm(dev.handle, rv.data_ptr(), xv.data_ptr(), 1.0,
+                                        ids.data_ptr(), 1, stream_handle()))
+    else:
+        _lib.check(dev._lib.dg_patch_fdm(dev.handle, rv.data_ptr(), xv.data_ptr(), 1.0,
+                                         ids.data_ptr(), 1, 0, stream_handle()))
+    out = xv[idx].cpu().numpy()
+    return out.reshape(shape)
 
 
 class Selection:
@@ -113,7 +154,10 @@ class _SolverSetBase:
         self.classes = []
         for code in np.unique(class_of):
             rows = np.nonzero(class_of == code)[0].astype(np.int64)
-            self.classes.append((rows, self._solver_for(int(code))))
+            solver = self._solver_for(int(code))
+            solver._set = self
+            solver._rep = int(rows[0])
+            self.classes.append((rows, solver))
         if self.counter is not None:
             self.counter.add("smoother_setup", len(self.classes) * local_solver_setup_flops(
                 self.dim, self.ctx.basis.degree, "cell" if self.kind == "cell" else "vertex_patch"))

@@ -17,6 +17,13 @@ from oracle.sipg_oracle import OracleLevel
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _deterministic(monkeypatch):
+    # bitwise comparisons need the write-disjoint colour launches (the
+    # single-launch atomic AVS path sums overlaps in arbitrary order)
+    monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
+
+
 def _exchange(sms, attr="x"):
     for r, sm in enumerate(sms):
         for peer, _, recv in sm.layout.halo_plan():

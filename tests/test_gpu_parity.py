@@ -265,6 +265,7 @@ def test_dataflow_avs_kernel_bitwise_equals_colour_launches(d, nc, k, monkeypatc
     ctx, _, sm = _setup(d, nc, k, "avs", 0.25)
     x0, b = inputs(ctx.ndofs, 6)
     monkeypatch.setenv("DGB_CLUSTER", "0")
+    monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
     monkeypatch.setenv("DGB_FLOW", "0")
     xa = x0.copy()
     sm.smooth(xa, b)
@@ -284,6 +285,7 @@ def test_cluster_avs_matches_colour_launches_and_oracle(d, nc, k, monkeypatch):
     (cluster_kernel): same update, different summation order per DoF."""
     ctx, _, sm = _setup(d, nc, k, "avs", 0.25)
     x0, b = inputs(ctx.ndofs, 8)
+    monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
     monkeypatch.setenv("DGB_CLUSTER", "0")
     xa = x0.copy()
     sm.use_graph = False
@@ -294,3 +296,48 @@ def test_cluster_avs_matches_colour_launches_and_oracle(d, nc, k, monkeypatch):
     assert rel(xb - x0, xa - x0) <= 1e-13
     want = OracleLevel((nc,) * d, k).smooth("avs", 0.25, x0, b)
     assert rel(xb, want) <= RTOL
+
+
+@pytest.mark.parametrize("d,nc,k", [(3, 12, 3), (2, 21, 4), (3, 5, 7)])
+def test_single_launch_atomic_avs_matches_colour_launches(d, nc, k, monkeypatch):
+    """Small levels run the additive patch step as one launch with fp64
+    reductions (DGB_AVS_ATOMIC); equal to the colour launches up to rounding."""
+    ctx, _, sm = _setup(d, nc, k, "avs", 0.25)
+    sm.use_graph = False
+    x0, b = inputs(ctx.ndofs, 9)
+    monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
+    xa = x0.copy()
+    sm.smooth(xa, b)
+    monkeypatch.setenv("DGB_AVS_ATOMIC", "1")
+    xb = x0.copy()
+    sm.smooth(xb, b)
+    assert ctx.dev._lib.dg_last_launch_count(ctx.dev.handle) == 2
+    assert rel(xb - x0, xa - x0) <= 1e-13
+
+
+def test_local_solver_apply_inverse_is_exact_local_solve():
+    """`LocalSolver.apply_inverse` (fastdiag.py:118-133) on the device: the
+    cell solver inverts the Kronecker-sum cell matrix, the patch solver the
+    dense patch restriction of the operator (oracle dense matrix)."""
+    lvl = dg.build_hierarchy(3, 3, 0).levels[0]
+    basis = dg.Basis1D.make(2)
+    ctx = dg.make_context(lvl, basis)
+    ol = OracleLevel((3, 3, 3), 2)
+    a = ol.dense()
+    rng = np.random.default_rng(12)
+    cset = fd.CellSolverSet(lvl, basis, 1.0, ctx=ctx)
+    for cell in (0, 13, 26):
+        solver = cset.local_solver(cell)
+        idx = np.arange(cell * 27, (cell + 1) * 27)
+        r = rng.standard_normal(27)
+        want = np.linalg.solve(a[np.ix_(idx, idx)], r)
+        assert rel(solver.apply_inverse(r), want) <= 1e-12
+        assert rel(fd.apply_inverse(solver, r.reshape(3, 3, 3)).ravel(), want) <= 1e-12
+    pset = fd.PatchSolverSet(lvl, basis, 1.0, ctx=ctx)
+    for j in range(len(pset.patches)):
+        idx = pset.subdomain_indices(j)
+        r = rng.standard_normal(idx.size)
+        want = np.linalg.solve(a[np.ix_(idx, idx)], r)
+        assert rel(pset.local_solver(j).apply_inverse(r), want) <= 1e-12
+    with pytest.raises(ValueError):
+        cset.local_solver(0).apply_inverse(np.zeros(5))
