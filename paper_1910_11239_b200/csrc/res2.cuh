@@ -69,28 +69,42 @@ __device__ __forceinline__ int res_cell(const Geo& geo, const int32_t* list, int
   return cell;
 }
 
-// G_t fiber: A_diag(digit) along t plus the rank-2 neighbour couplings
+// G_t fiber: A_diag(digit) along t plus the rank-2 neighbour couplings.  The
+// neighbour fibers are reduced to their face value and normal derivative
+// before the own fiber is loaded, so at most one fiber-sized array of
+// neighbour data is live (register budget at n = 16).
 template <int D, int N>
 __device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, int f,
                                              const int* c, const double* X, double* out) {
   using L = Lay<D, N>;
   const int sb = L::sbase(t, f), ss = L::sstride(t);
   const int digit = (c[t] == 0 ? 1 : 0) | (c[t] == p.geo.nc[t] - 1 ? 2 : 0);
-  // neighbour fibers first (global loads in flight during the matvec)
   const int gb = L::gbase(t, f), gs = L::gstride(t);
-  double xr[N], xl[N];
   int nb[3] = {c[0], c[1], D == 3 ? c[2] : 0};
-  if (!(digit & 2)) {
+  double r_hi = 0.0, r_all = 0.0, l_lo = 0.0, l_all = 0.0;
+  if (!(digit & 2)) {  // a_pm x_R: value and normal derivative at the shared face
     nb[t] = c[t] + 1;
     const double* q = p.x + (int64_t)cell_local<D>(p.geo, nb) * L::NE + gb;
+    double xr[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) xr[k] = __ldg(q + k * gs);
+    double g = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) g = fma(p.mats.bg0[k], xr[k], g);
+    r_all = p.betap * xr[0];
+    r_hi = p.alpha * xr[0] + p.beta * g;
   }
-  if (!(digit & 1)) {
+  if (!(digit & 1)) {  // a_pm^T x_L
     nb[t] = c[t] - 1;
     const double* q = p.x + (int64_t)cell_local<D>(p.geo, nb) * L::NE + gb;
+    double xl[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) xl[k] = __ldg(q + k * gs);
+    double g = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) g = fma(p.mats.bg1[k], xl[k], g);
+    l_all = p.beta * xl[N - 1];
+    l_lo = p.alpha * xl[N - 1] + p.betap * g;
   }
   double v[N], o[N];
 #pragma unroll
@@ -101,23 +115,15 @@ __device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, i
   } else {
     matvec_digit<N>(p.mats.adiag, digit, v, o);
   }
-  if (!(digit & 2)) {  // a_pm x_R: value and normal derivative at the shared face
-    double g = 0.0;
+  if (!(digit & 2)) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) g = fma(p.mats.bg0[k], xr[k], g);
-    const double fall = p.betap * xr[0];
-#pragma unroll
-    for (int i = 0; i < N; ++i) o[i] = fma(p.mats.bg1[i], fall, o[i]);
-    o[N - 1] += p.alpha * xr[0] + p.beta * g;
+    for (int i = 0; i < N; ++i) o[i] = fma(p.mats.bg1[i], r_all, o[i]);
+    o[N - 1] += r_hi;
   }
-  if (!(digit & 1)) {  // a_pm^T x_L
-    double g = 0.0;
+  if (!(digit & 1)) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) g = fma(p.mats.bg1[k], xl[k], g);
-    const double fall = p.beta * xl[N - 1];
-#pragma unroll
-    for (int i = 0; i < N; ++i) o[i] = fma(p.mats.bg0[i], fall, o[i]);
-    o[0] += p.alpha * xl[N - 1] + p.betap * g;
+    for (int i = 0; i < N; ++i) o[i] = fma(p.mats.bg0[i], l_all, o[i]);
+    o[0] += l_lo;
   }
 #pragma unroll
   for (int i = 0; i < N; ++i) out[sb + i * ss] = o[i];
