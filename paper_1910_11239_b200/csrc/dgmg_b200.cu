@@ -9,9 +9,7 @@
 //  - the smoothing-step launch sequences of LevelSmoother (smoothers.py:
 //    131-166), captured once into CUDA graphs and replayed.
 #include "../../include/dgmg_b200.h"
-#include "common.cuh"
-#include "fdm2.cuh"
-#include "res2.cuh"
+#include "launch.h"
 #include "flow.cuh"
 
 #include <cstdlib>
@@ -27,19 +25,13 @@
 
 namespace dgb {
 
-static thread_local std::string g_err;
+thread_local std::string g_err;
 
-static int fail(int code, const std::string& msg) {
+int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
 
-#define DG_CUDA(call)                                                        \
-  do {                                                                       \
-    cudaError_t e_ = (call);                                                 \
-    if (e_ != cudaSuccess)                                                   \
-      return fail(DG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
 
 __global__ void gather_map_kernel(MapParams p) {
   const int64_t per = (p.d == 3) ? (int64_t)p.m * p.m * p.m : (int64_t)p.m * p.m;
@@ -70,281 +62,6 @@ __global__ void gather_map_kernel(MapParams p) {
 // ---------------------------------------------------------------------------
 // template dispatch
 // ---------------------------------------------------------------------------
-// host-side launch arguments (the kernels' parameter structs are built from these)
-struct ResArgs {
-  const double* x = nullptr;
-  const double* b = nullptr;
-  double* r = nullptr;
-  const int32_t* list = nullptr;
-  int64_t start = 0;
-  int64_t count = 0;
-  int packed = 0;
-  double alpha = 0, beta = 0, betap = 0;
-  Geo geo;
-};
-
-struct FdmArgs {
-  const double* r = nullptr;
-  double* x = nullptr;
-  const int32_t* list = nullptr;
-  int64_t start = 0;
-  int64_t count = 0;
-  int packed = 0;
-  int atomic = 0;
-  int cluster = 0;  // list holds cluster base vertices (cluster_kernel)
-  int pv_lo = 0, pv_hi = 0;
-  const double* invsum = nullptr;
-  double omega = 0;
-  Geo geo;
-};
-
-static int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e && *e ? std::atoi(e) : dflt;
-}
-
-template <typename K>
-static int resident_ctas(K k, int threads, size_t smem, int* out) {
-  int per_sm = 0, dev = 0, sms = 0;
-  DG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem));
-  DG_CUDA(cudaGetDevice(&dev));
-  DG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  *out = std::max(1, per_sm) * sms;
-  return DG_OK;
-}
-
-struct HostRes {
-  const double* mass;   // n*n
-  const double* adiag;  // 4*n*n
-  const double* bg;     // 2*n
-  const double* eo;     // 4*(n/2)^2 or nullptr
-};
-
-template <int D, int N>
-static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) {
-  if (q.count <= 0) return DG_OK;
-  constexpr int G = fdm2_groups<D, N>();
-  constexpr int NT = G * Lay<D, N>::F;
-  Res2Params<D, N> p;
-  p.x = q.x;
-  p.b = q.b;
-  p.r = q.r;
-  p.list = q.list;
-  p.start = q.start;
-  p.count = q.count;
-  p.packed = q.packed;
-  p.alpha = q.alpha;
-  p.beta = q.beta;
-  p.betap = q.betap;
-  p.geo = q.geo;
-  for (int i = 0; i < N; ++i)
-    for (int k = 0; k < N; ++k) {
-      p.mats.mass[k * N + i] = h.mass[i * N + k];
-      for (int dg = 0; dg < 4; ++dg) p.mats.adiag[dg][k * N + i] = h.adiag[dg * N * N + i * N + k];
-    }
-  std::memcpy(p.mats.bg0, h.bg, sizeof(p.mats.bg0));
-  std::memcpy(p.mats.bg1, h.bg + N, sizeof(p.mats.bg1));
-  p.eo = h.eo != nullptr && N % 2 == 0;
-  if (p.eo) std::memcpy(p.mats.eo, h.eo, sizeof(p.mats.eo));
-  const int64_t ngroups = (q.count + G - 1) / G;
-  const size_t smem = sizeof(double) * res2_smem_doubles<D, N>();
-  auto k = res2_kernel<D, N>;
-  static bool attr = false;
-  if (!attr) {
-    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
-  k<<<(unsigned)ngroups, NT, smem, st>>>(p);
-  DG_CUDA(cudaGetLastError());
-  return DG_OK;
-}
-
-template <int D, int M, bool PATCH>
-static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, const double* heo,
-                      cudaStream_t st) {
-  if (q.count <= 0) return DG_OK;
-  constexpr int G = fdm2_groups<D, M>();
-  Fdm2Params<D, M> p;
-  p.r = q.r;
-  p.x = q.x;
-  p.list = q.list;
-  p.start = q.start;
-  p.count = q.count;
-  p.invsum = q.invsum;
-  p.omega = q.omega;
-  p.atomic = q.atomic;
-  p.packed = q.packed;
-  p.geo = q.geo;
-  // fwd[k][i] = Z[k][i] (out = Z^T v); bwd[k][i] = Z^T[k][i] (out = Z v)
-  std::memcpy(p.mats.fwd, hz, sizeof(p.mats.fwd));
-  std::memcpy(p.mats.bwd, hzt, sizeof(p.mats.bwd));
-  p.eo = heo != nullptr && M % 2 == 0;
-  if (p.eo) std::memcpy(p.mats.eo, heo, sizeof(p.mats.eo));
-  p.pv_lo = q.pv_lo;
-  p.pv_hi = q.pv_hi;
-  const int64_t ngroups = (q.count + G - 1) / G;
-  if (!q.atomic && !q.cluster && env_int("DGB_FDM", 2) == 5) {
-    using S5 = Fdm5Shape<D, M, PATCH>;
-    const size_t smem5 = sizeof(double) * S5::SMEM;
-    auto k5 = fdm5_kernel<D, M, PATCH>;
-    static int resident = 0;
-    if (!resident) {
-      DG_CUDA(cudaFuncSetAttribute(k5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
-      if (int rc = resident_ctas(k5, S5::NT, smem5, &resident)) return rc;
-    }
-    k5<<<(unsigned)std::min<int64_t>(ngroups, resident), S5::NT, smem5, st>>>(p, ngroups);
-    DG_CUDA(cudaGetLastError());
-    return DG_OK;
-  }
-  const size_t smem = sizeof(double) * fdm2_smem_doubles<D, M>();
-  if constexpr (PATCH) {
-    if (q.cluster) {
-      auto kc = cluster_kernel<D, M>;
-      static bool attr_c = false;
-      if (!attr_c) {
-        DG_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_c = true;
-      }
-      kc<<<(unsigned)ngroups, G * Lay<D, M>::F, smem, st>>>(p);
-      DG_CUDA(cudaGetLastError());
-      return DG_OK;
-    }
-  }
-  auto k = fdm2_kernel<D, M, PATCH>;
-  static bool attr = false;
-  if (!attr) {
-    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
-  k<<<(unsigned)ngroups, G * Lay<D, M>::F, smem, st>>>(p);
-  DG_CUDA(cudaGetLastError());
-  return DG_OK;
-}
-
-struct FlowDev {
-  FlowTask* tasks = nullptr;
-  int32_t* succ = nullptr;
-  int32_t* plist = nullptr;
-  int* state = nullptr;       // live scheduler state
-  int* state_init = nullptr;  // its initial image (copied in before each step)
-  int ntasks = 0;
-  int64_t units = 0;
-};
-
-template <int D, int N>
-static int launch_flow(const ResArgs& ra, const FdmArgs& fa, const HostRes& h, const double* hz,
-                       const double* hzt, const double* heo, const FlowDev& fd, cudaStream_t st) {
-  using S = FlowShape<D, N>;
-  constexpr int M = 2 * N;
-  const size_t smem = sizeof(double) * S::SMEM;
-  auto k = flow_kernel<D, N>;
-  static int resident = 0;
-  if (!resident) {
-    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (int rc = resident_ctas(k, S::NT, smem, &resident)) return rc;
-  }
-  FlowParams<D, N> p;
-  Res2Params<D, N>& r = p.res;
-  r.x = ra.x;
-  r.b = ra.b;
-  r.r = ra.r;
-  r.list = nullptr;
-  r.start = 0;
-  r.count = 0;
-  r.packed = 0;
-  r.alpha = ra.alpha;
-  r.beta = ra.beta;
-  r.betap = ra.betap;
-  r.geo = ra.geo;
-  for (int i = 0; i < N; ++i)
-    for (int kk = 0; kk < N; ++kk) {
-      r.mats.mass[kk * N + i] = h.mass[i * N + kk];
-      for (int dg = 0; dg < 4; ++dg) r.mats.adiag[dg][kk * N + i] = h.adiag[dg * N * N + i * N + kk];
-    }
-  std::memcpy(r.mats.bg0, h.bg, sizeof(r.mats.bg0));
-  std::memcpy(r.mats.bg1, h.bg + N, sizeof(r.mats.bg1));
-  r.eo = h.eo != nullptr && N % 2 == 0;
-  if (r.eo) std::memcpy(r.mats.eo, h.eo, sizeof(r.mats.eo));
-  Fdm2Params<D, M>& f = p.fdm;
-  f.r = fa.r;
-  f.x = fa.x;
-  f.list = nullptr;
-  f.start = 0;
-  f.count = 0;
-  f.invsum = fa.invsum;
-  f.omega = fa.omega;
-  f.atomic = 0;
-  f.packed = 1;
-  f.geo = fa.geo;
-  std::memcpy(f.mats.fwd, hz, sizeof(f.mats.fwd));
-  std::memcpy(f.mats.bwd, hzt, sizeof(f.mats.bwd));
-  f.eo = heo != nullptr;
-  if (f.eo) std::memcpy(f.mats.eo, heo, sizeof(f.mats.eo));
-  p.tasks = fd.tasks;
-  p.succ = fd.succ;
-  p.plist = fd.plist;
-  p.state = fd.state;
-  p.ntasks = fd.ntasks;
-  DG_CUDA(cudaMemcpyAsync(fd.state, fd.state_init, sizeof(int) * (4 + 5 * (size_t)fd.ntasks),
-                          cudaMemcpyDeviceToDevice, st));
-  k<<<(unsigned)std::min<int64_t>(fd.units, resident), S::NT, smem, st>>>(p);
-  DG_CUDA(cudaGetLastError());
-  return DG_OK;
-}
-
-static bool flow_shape(int d, int n, int* gp, int* gr) {
-#define X(D, N) \
-  if (d == D && n == N) { *gp = FlowShape<D, N>::GP; *gr = FlowShape<D, N>::GR; return true; }
-  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
-  X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 6) X(3, 7) X(3, 8)
-#undef X
-  return false;
-}
-
-static int dispatch_flow(int d, int n, const ResArgs& ra, const FdmArgs& fa, const HostRes& h,
-                         const double* hz, const double* hzt, const double* heo,
-                         const FlowDev& fd, cudaStream_t st) {
-#define X(D, N) if (d == D && n == N) return launch_flow<D, N>(ra, fa, h, hz, hzt, heo, fd, st);
-  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
-  X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 6) X(3, 7) X(3, 8)
-#undef X
-  return fail(DG_EUNSUPPORTED, "flow: no kernel");
-}
-
-#define DG_N_CASES(X, D) \
-  X(D, 2) X(D, 3) X(D, 4) X(D, 5) X(D, 6) X(D, 7) X(D, 8) X(D, 9) X(D, 10) \
-  X(D, 11) X(D, 12) X(D, 13) X(D, 14) X(D, 15) X(D, 16)
-
-static int dispatch_residual(int d, int n, const ResArgs& p, const HostRes& h,
-                             cudaStream_t st) {
-#define X(D, N) if (d == D && n == N) return launch_residual<D, N>(p, h, st);
-  DG_N_CASES(X, 2)
-  DG_N_CASES(X, 3)
-#undef X
-  return fail(DG_EUNSUPPORTED, "residual: no kernel for dim " + std::to_string(d) +
-                                   ", n " + std::to_string(n));
-}
-
-static int dispatch_cell_fdm(int d, int n, const FdmArgs& p, const double* hz,
-                             const double* hzt, const double* heo, cudaStream_t st) {
-#define X(D, N) if (d == D && n == N) return launch_fdm<D, N, false>(p, hz, hzt, heo, st);
-  DG_N_CASES(X, 2)
-  DG_N_CASES(X, 3)
-#undef X
-  return fail(DG_EUNSUPPORTED, "cell fdm: no kernel for dim " + std::to_string(d) +
-                                   ", n " + std::to_string(n));
-}
-
-static int dispatch_patch_fdm(int d, int n, const FdmArgs& p, const double* hz,
-                              const double* hzt, const double* heo, cudaStream_t st) {
-#define X(D, N) if (d == D && n == N) return launch_fdm<D, 2 * N, true>(p, hz, hzt, heo, st);
-  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
-  X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 6) X(3, 7) X(3, 8)
-#undef X
-  return fail(DG_EUNSUPPORTED, "patch fdm: no kernel for dim " + std::to_string(d) +
-                                   ", degree " + std::to_string(n - 1) +
-                                   " (vertex patches support k <= 7)");
-}
 
 }  // namespace dgb
 
@@ -444,6 +161,8 @@ static FdmArgs fdm_params(const dg_level* L, bool patch, const double* r, double
   p.r = r;
   p.x = x;
   p.invsum = patch ? L->pinv : L->cinv;
+  p.zd = patch ? L->pz : L->cz;
+  p.ztd = patch ? L->pzt : L->czt;
   p.omega = omega;
   p.geo = L->geo;
   return p;

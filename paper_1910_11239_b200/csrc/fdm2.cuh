@@ -46,6 +46,7 @@ struct Fdm2Params {
   int packed;   // list entries are packed global coordinates (pack3)
   int eo;       // interior digit uses the even/odd halves
   int pv_lo, pv_hi;  // cluster mode: patch vertices v_d outside are skipped
+  int direct;   // first/last contraction straight from/to global rows (no gather/scatter pass)
   Geo geo;
   FdmMats<M> mats;
 };
@@ -314,6 +315,67 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int K>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
 
+// Direction-0 fiber f of a subdomain as global cell rows: the fiber is the
+// row (j1 % N, j2 % N) of the cell slots h + 2 (j1 / N) + 4 (j2 / N), h = 0, 1
+// (patches), or one row of the single cell.  goff = row offset in the cell.
+template <int D, int M, bool PATCH>
+__device__ __forceinline__ void fiber_rows(int f, int& slot0, int& goff) {
+  constexpr int N = PATCH ? M / 2 : M;
+  const int j1 = (D == 3) ? f % M : f, j2 = (D == 3) ? f / M : 0;
+  if (PATCH) {
+    slot0 = 2 * (j1 / N) + ((D == 3) ? 4 * (j2 / N) : 0);
+    goff = ((j1 % N) + ((D == 3) ? N * (j2 % N) : 0)) * N;
+  } else {
+    slot0 = 0;
+    goff = (j1 + ((D == 3) ? N * j2 : 0)) * N;
+  }
+}
+
+template <int N, int M>
+__device__ __forceinline__ void rows_to_reg(double (&v)[M], int h, const double* __restrict__ g,
+                                            bool coherent) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      const double2 t = coherent ? __ldcg(reinterpret_cast<const double2*>(g + i))
+                                 : __ldg(reinterpret_cast<const double2*>(g + i));
+      v[h * N + i] = t.x;
+      v[h * N + i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[h * N + i] = coherent ? __ldcg(g + i) : __ldg(g + i);
+  }
+}
+
+template <int N, int M>
+__device__ __forceinline__ void reg_update(double* __restrict__ g, const double (&o)[M], int h,
+                                           double omega, int atomic, bool coherent) {
+  if (atomic) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) atomicAdd(g + i, omega * o[h * N + i]);
+    return;
+  }
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+      double2 t = coherent ? __ldcg(reinterpret_cast<const double2*>(g + i))
+                           : *reinterpret_cast<const double2*>(g + i);
+      t.x = fma(omega, o[h * N + i], t.x);
+      t.y = fma(omega, o[h * N + i + 1], t.y);
+      if (coherent) __stcg(reinterpret_cast<double2*>(g + i), t);
+      else *reinterpret_cast<double2*>(g + i) = t;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double t = coherent ? __ldcg(g + i) : g[i];
+      if (coherent) __stcg(g + i, fma(omega, o[h * N + i], t));
+      else g[i] = fma(omega, o[h * N + i], t);
+    }
+  }
+}
+
 // rows of a subdomain: (cell slot, i1, i2) -> (global offset, shared offset)
 template <int D, int M, bool PATCH>
 struct Rows {
@@ -385,23 +447,42 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     }
   }
   __syncthreads();
-  // gather R_j r, one cell row per thread iteration
-  for (int row = tid; row < G * R::RPS; row += NT) {
-    const int g = row / R::RPS;
-    if (!s_info[g][7]) continue;
-    int slot, goff, soff;
-    R::map(row - g * R::RPS, slot, goff, soff);
-    if (coherent) row_load_cg<N>(sm + g * L::SZ + soff, p.r + s_cell[g][slot] + goff);
-    else row_load<N>(sm + g * L::SZ + soff, p.r + s_cell[g][slot] + goff);
-  }
-  __syncthreads();
   const int g = tid / F, f = tid - (tid / F) * F;
   const bool active = s_info[g][7];
   const int* dg = s_info[g];
   double* buf = sm + g * L::SZ;
-  // forward contractions with Z^T, directions 0 .. D-2
+  constexpr int H = PATCH ? 2 : 1;  // cell rows per direction-0 fiber
+  int slot0 = 0, goff = 0;
+  fiber_rows<D, M, PATCH>(f, slot0, goff);
+  if (p.direct) {
+    // first forward contraction (direction 0) straight from the global rows of R_j r
+    if (active) {
+      double v[M], o[M];
 #pragma unroll
-  for (int t = 0; t < D - 1; ++t) {
+      for (int h = 0; h < H; ++h) rows_to_reg<N, M>(v, h, p.r + s_cell[g][slot0 + h] + goff, coherent);
+      fdm_matvec<M, true>(p.mats, p.eo, dg[0], v, o);
+      const int sb = L::sbase(0, f);
+#pragma unroll
+      for (int k = 0; k < M; ++k) buf[sb + k] = o[k];
+    }
+    __syncthreads();
+  } else {
+    // gather R_j r, one cell row per thread iteration
+    for (int row = tid; row < G * R::RPS; row += NT) {
+      const int gg = row / R::RPS;
+      if (!s_info[gg][7]) continue;
+      int slot, go, soff;
+      R::map(row - gg * R::RPS, slot, go, soff);
+      if (coherent) row_load_cg<N>(sm + gg * L::SZ + soff, p.r + s_cell[gg][slot] + go);
+      else row_load<N>(sm + gg * L::SZ + soff, p.r + s_cell[gg][slot] + go);
+    }
+    __syncthreads();
+    if (active) fdm_fiber<M, true>(p.mats, p.eo, dg[0], buf, L::sbase(0, f), L::sstride(0));
+    __syncthreads();
+  }
+  // forward contractions with Z^T, directions 1 .. D-2
+#pragma unroll
+  for (int t = 1; t < D - 1; ++t) {
     if (active) fdm_fiber<M, true>(p.mats, p.eo, dg[t], buf, L::sbase(t, f), L::sstride(t));
     __syncthreads();
   }
@@ -421,22 +502,38 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     for (int k = 0; k < M; ++k) buf[sb + k * ss] = v[k];
   }
   __syncthreads();
-  // backward contractions with Z, directions D-2 .. 0
+  // backward contractions with Z, directions D-2 .. 1
 #pragma unroll
-  for (int s = 0; s < D - 1; ++s) {
+  for (int s = 0; s < D - 2; ++s) {
     const int t = D - 2 - s;
     if (active) fdm_fiber<M, false>(p.mats, p.eo, dg[t], buf, L::sbase(t, f), L::sstride(t));
     __syncthreads();
   }
+  if (p.direct) {
+    // last backward contraction (direction 0) and x += omega R_j^T y from registers
+    if (active) {
+      double v[M], o[M];
+      const int sb = L::sbase(0, f);
+#pragma unroll
+      for (int k = 0; k < M; ++k) v[k] = buf[sb + k];
+      fdm_matvec<M, false>(p.mats, p.eo, dg[0], v, o);
+#pragma unroll
+      for (int h = 0; h < H; ++h)
+        reg_update<N, M>(p.x + s_cell[g][slot0 + h] + goff, o, h, p.omega, p.atomic, coherent);
+    }
+    return;
+  }
+  if (active) fdm_fiber<M, false>(p.mats, p.eo, dg[0], buf, L::sbase(0, f), L::sstride(0));
+  __syncthreads();
   // scatter-add omega * R_j^T y, one cell row per thread iteration
   for (int row = tid; row < G * R::RPS; row += NT) {
     const int gg = row / R::RPS;
     if (!s_info[gg][7]) continue;
-    int slot, goff, soff;
-    R::map(row - gg * R::RPS, slot, goff, soff);
-    if (p.atomic) row_red<N>(p.x + s_cell[gg][slot] + goff, sm + gg * L::SZ + soff, p.omega);
-    else if (coherent) row_update_cg<N>(p.x + s_cell[gg][slot] + goff, sm + gg * L::SZ + soff, p.omega);
-    else row_update<N>(p.x + s_cell[gg][slot] + goff, sm + gg * L::SZ + soff, p.omega, false);
+    int slot, go, soff;
+    R::map(row - gg * R::RPS, slot, go, soff);
+    if (p.atomic) row_red<N>(p.x + s_cell[gg][slot] + go, sm + gg * L::SZ + soff, p.omega);
+    else if (coherent) row_update_cg<N>(p.x + s_cell[gg][slot] + go, sm + gg * L::SZ + soff, p.omega);
+    else row_update<N>(p.x + s_cell[gg][slot] + go, sm + gg * L::SZ + soff, p.omega, false);
   }
 }
 
@@ -446,6 +543,27 @@ fdm2_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
   extern __shared__ double sm[];
   fdm_group<D, M, PATCH, fdm2_groups<D, M>()>(p, p.list, p.packed, p.start, p.count, blockIdx.x,
                                               sm, false);
+}
+
+// fdm6: persistent variant of fdm2 with staggered starts.  All CTAs of a
+// launch have the same work, so in fdm2 every wave gathers, contracts and
+// scatters in lock-step and the memory and DFMA phases of co-resident CTAs do
+// not overlap.  Here the k-th CTA slot of each SM starts k * stagger_ns late
+// and then walks its groups back to back, keeping the phases interleaved.
+template <int D, int M, bool PATCH>
+__global__ void __launch_bounds__(fdm2_groups<D, M>() * Lay<D, M>::F)
+fdm6_kernel(const __grid_constant__ Fdm2Params<D, M> p, int64_t ngroups, int stagger_ns,
+            int nsm) {
+  extern __shared__ double sm[];
+  if (stagger_ns > 0) {
+    const int slot = (int)(blockIdx.x / nsm);
+    for (int i = 0; i < slot; ++i) __nanosleep(stagger_ns);
+  }
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    fdm_group<D, M, PATCH, fdm2_groups<D, M>()>(p, p.list, p.packed, p.start, p.count, grp, sm,
+                                                false);
+    __syncthreads();
+  }
 }
 
 

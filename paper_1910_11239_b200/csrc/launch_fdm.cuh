@@ -1,0 +1,107 @@
+// launch_fdm.cuh - host launch of the local-solve kernels (fdm2.cuh,
+// fdm_mma.cuh); instantiated by launch_fdm_cell.cu / launch_fdm_patch.cu.
+#pragma once
+#include "launch.h"
+#include "fdm2.cuh"
+#include "fdm_mma.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+namespace dgb {
+
+template <int D, int M, bool PATCH>
+static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, const double* heo,
+                      cudaStream_t st) {
+  if (q.count <= 0) return DG_OK;
+  constexpr int G = fdm2_groups<D, M>();
+  Fdm2Params<D, M> p;
+  p.r = q.r;
+  p.x = q.x;
+  p.list = q.list;
+  p.start = q.start;
+  p.count = q.count;
+  p.invsum = q.invsum;
+  p.omega = q.omega;
+  p.atomic = q.atomic;
+  p.packed = q.packed;
+  p.geo = q.geo;
+  // fwd[k][i] = Z[k][i] (out = Z^T v); bwd[k][i] = Z^T[k][i] (out = Z v)
+  std::memcpy(p.mats.fwd, hz, sizeof(p.mats.fwd));
+  std::memcpy(p.mats.bwd, hzt, sizeof(p.mats.bwd));
+  p.eo = heo != nullptr && M % 2 == 0;
+  if (p.eo) std::memcpy(p.mats.eo, heo, sizeof(p.mats.eo));
+  p.pv_lo = q.pv_lo;
+  p.pv_hi = q.pv_hi;
+  p.direct = env_int("DGB_DIRECT", 1);
+  if constexpr (D == 3 && M % 8 == 0) {
+    // fp64 tensor cores (fdm_mma.cuh) for m = 8, 16
+    if (!q.cluster && q.zd && q.ztd && env_int("DGB_MMA", 0)) {
+      using S = MmaShape<M, PATCH>;
+      const size_t smem = sizeof(double) * S::SMEM;
+      auto k = fdm_mma_kernel<M, PATCH>;
+      static bool attr = false;
+      if (!attr) {
+        DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+      }
+      k<<<(unsigned)((q.count + S::GS - 1) / S::GS), S::NT, smem, st>>>(p, q.zd, q.ztd);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
+  }
+  const int64_t ngroups = (q.count + G - 1) / G;
+  if (!q.atomic && !q.cluster && env_int("DGB_FDM", 2) == 5) {
+    using S5 = Fdm5Shape<D, M, PATCH>;
+    const size_t smem5 = sizeof(double) * S5::SMEM;
+    auto k5 = fdm5_kernel<D, M, PATCH>;
+    static int resident = 0;
+    if (!resident) {
+      DG_CUDA(cudaFuncSetAttribute(k5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
+      if (int rc = resident_ctas(k5, S5::NT, smem5, &resident)) return rc;
+    }
+    k5<<<(unsigned)std::min<int64_t>(ngroups, resident), S5::NT, smem5, st>>>(p, ngroups);
+    DG_CUDA(cudaGetLastError());
+    return DG_OK;
+  }
+  const size_t smem = sizeof(double) * fdm2_smem_doubles<D, M>();
+  if constexpr (PATCH) {
+    if (q.cluster) {
+      auto kc = cluster_kernel<D, M>;
+      static bool attr_c = false;
+      if (!attr_c) {
+        DG_CUDA(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_c = true;
+      }
+      kc<<<(unsigned)ngroups, G * Lay<D, M>::F, smem, st>>>(p);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
+  }
+  if (!q.cluster && env_int("DGB_FDM", 2) == 6) {
+    auto k6 = fdm6_kernel<D, M, PATCH>;
+    static int resident = 0, nsm = 0;
+    if (!resident) {
+      DG_CUDA(cudaFuncSetAttribute(k6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (int rc = resident_ctas(k6, G * Lay<D, M>::F, smem, &resident)) return rc;
+      int dev = 0;
+      DG_CUDA(cudaGetDevice(&dev));
+      DG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    k6<<<(unsigned)std::min<int64_t>(ngroups, resident), G * Lay<D, M>::F, smem, st>>>(
+        p, ngroups, env_int("DGB_STAGGER", 2000), nsm);
+    DG_CUDA(cudaGetLastError());
+    return DG_OK;
+  }
+  auto k = fdm2_kernel<D, M, PATCH>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k<<<(unsigned)ngroups, G * Lay<D, M>::F, smem, st>>>(p);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
+}  // namespace dgb

@@ -1,0 +1,59 @@
+// launch_res.cu - residual kernels (res2.cuh), all (dim, n) instantiations.
+#include "launch.h"
+#include "res2.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+namespace dgb {
+
+template <int D, int N>
+static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) {
+  if (q.count <= 0) return DG_OK;
+  constexpr int G = fdm2_groups<D, N>();
+  constexpr int NT = G * Lay<D, N>::F;
+  Res2Params<D, N> p;
+  p.x = q.x;
+  p.b = q.b;
+  p.r = q.r;
+  p.list = q.list;
+  p.start = q.start;
+  p.count = q.count;
+  p.packed = q.packed;
+  p.alpha = q.alpha;
+  p.beta = q.beta;
+  p.betap = q.betap;
+  p.geo = q.geo;
+  for (int i = 0; i < N; ++i)
+    for (int k = 0; k < N; ++k) {
+      p.mats.mass[k * N + i] = h.mass[i * N + k];
+      for (int dg = 0; dg < 4; ++dg) p.mats.adiag[dg][k * N + i] = h.adiag[dg * N * N + i * N + k];
+    }
+  std::memcpy(p.mats.bg0, h.bg, sizeof(p.mats.bg0));
+  std::memcpy(p.mats.bg1, h.bg + N, sizeof(p.mats.bg1));
+  p.eo = h.eo != nullptr && N % 2 == 0;
+  if (p.eo) std::memcpy(p.mats.eo, h.eo, sizeof(p.mats.eo));
+  const int64_t ngroups = (q.count + G - 1) / G;
+  const size_t smem = sizeof(double) * res2_smem_doubles<D, N>();
+  auto k = res2_kernel<D, N>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k<<<(unsigned)ngroups, NT, smem, st>>>(p);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
+int dispatch_residual(int d, int n, const ResArgs& p, const HostRes& h,
+                             cudaStream_t st) {
+#define X(D, N) if (d == D && n == N) return launch_residual<D, N>(p, h, st);
+  DG_N_CASES(X, 2)
+  DG_N_CASES(X, 3)
+#undef X
+  return fail(DG_EUNSUPPORTED, "residual: no kernel for dim " + std::to_string(d) +
+                                   ", n " + std::to_string(n));
+}
+
+}  // namespace dgb
