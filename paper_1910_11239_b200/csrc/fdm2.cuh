@@ -395,8 +395,23 @@ struct Rows {
   }
 };
 
+template <int D, int G>
+__host__ __device__ constexpr bool fdm_interleave() {
+  return D == 3 && G > 1 && 16 % G == 0;
+}
+
+// doubles between the G subdomain tensors of a CTA: == 16/G (mod 16) when
+// the fused pass interleaves the subdomains, so that its 16 threads of a
+// half-warp (16/G fibers x G subdomains) hit 16 distinct 8-byte banks
+template <int D, int M, int G>
+__host__ __device__ constexpr int fdm_gstride() {
+  constexpr int SZ = Lay<D, M>::SZ;
+  if (!fdm_interleave<D, G>()) return SZ;
+  return SZ + ((16 / G - SZ % 16) % 16 + 16) % 16;
+}
+
 // one group of G subdomains (work items grp*G .. grp*G+G-1); all G*F threads
-// of the CTA take part; `sm` holds G*SZ doubles.  `coherent` reads r and x
+// of the CTA take part; `sm` holds G*fdm_gstride doubles.  `coherent` reads r and x
 // through L2 only (ld.cg) for use inside a kernel where other CTAs write them.
 template <int D, int M, bool PATCH, int G>
 __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32_t* list,
@@ -450,7 +465,8 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
   const int g = tid / F, f = tid - (tid / F) * F;
   const bool active = s_info[g][7];
   const int* dg = s_info[g];
-  double* buf = sm + g * L::SZ;
+  constexpr int GSZ = fdm_gstride<D, M, G>();
+  double* buf = sm + g * GSZ;
   constexpr int H = PATCH ? 2 : 1;  // cell rows per direction-0 fiber
   int slot0 = 0, goff = 0;
   fiber_rows<D, M, PATCH>(f, slot0, goff);
@@ -473,8 +489,8 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
       if (!s_info[gg][7]) continue;
       int slot, go, soff;
       R::map(row - gg * R::RPS, slot, go, soff);
-      if (coherent) row_load_cg<N>(sm + gg * L::SZ + soff, p.r + s_cell[gg][slot] + go);
-      else row_load<N>(sm + gg * L::SZ + soff, p.r + s_cell[gg][slot] + go);
+      if (coherent) row_load_cg<N>(sm + gg * GSZ + soff, p.r + s_cell[gg][slot] + go);
+      else row_load<N>(sm + gg * GSZ + soff, p.r + s_cell[gg][slot] + go);
     }
     __syncthreads();
     if (active) fdm_fiber<M, true>(p.mats, p.eo, dg[0], buf, L::sbase(0, f), L::sstride(0));
@@ -486,20 +502,28 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     if (active) fdm_fiber<M, true>(p.mats, p.eo, dg[t], buf, L::sbase(t, f), L::sstride(t));
     __syncthreads();
   }
-  // fused: Z^T along D-1, scale by 1/Lambda-sum, Z along D-1
-  if (active) {
-    constexpr int t = D - 1;
-    const int sb = L::sbase(t, f), ss = L::sstride(t);
-    const double* inv = p.invsum + (int64_t)dg[6] * L::NE + L::gbase(t, f);
-    double v[M], o[M];
+  // fused: Z^T along D-1, scale by 1/Lambda-sum, Z along D-1.  In 3D the
+  // threads take the G subdomains interleaved here (with the group stride of
+  // fdm_gstride the half-warp accesses of this strided pass are conflict free)
+  {
+    constexpr bool IL = fdm_interleave<D, G>();
+    const int gi = IL ? tid % G : g, fi = IL ? tid / G : f;
+    if (s_info[gi][7]) {
+      constexpr int t = D - 1;
+      const int* dgi = s_info[gi];
+      double* bufi = sm + gi * GSZ;
+      const int sb = L::sbase(t, fi), ss = L::sstride(t);
+      const double* inv = p.invsum + (int64_t)dgi[6] * L::NE + L::gbase(t, fi);
+      double v[M], o[M];
 #pragma unroll
-    for (int k = 0; k < M; ++k) v[k] = buf[sb + k * ss];
-    fdm_matvec<M, true>(p.mats, p.eo, dg[t], v, o);
+      for (int k = 0; k < M; ++k) v[k] = bufi[sb + k * ss];
+      fdm_matvec<M, true>(p.mats, p.eo, dgi[t], v, o);
 #pragma unroll
-    for (int k = 0; k < M; ++k) o[k] *= __ldg(inv + k * L::gstride(t));
-    fdm_matvec<M, false>(p.mats, p.eo, dg[t], o, v);
+      for (int k = 0; k < M; ++k) o[k] *= __ldg(inv + k * L::gstride(t));
+      fdm_matvec<M, false>(p.mats, p.eo, dgi[t], o, v);
 #pragma unroll
-    for (int k = 0; k < M; ++k) buf[sb + k * ss] = v[k];
+      for (int k = 0; k < M; ++k) bufi[sb + k * ss] = v[k];
+    }
   }
   __syncthreads();
   // backward contractions with Z, directions D-2 .. 1
@@ -531,9 +555,9 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     if (!s_info[gg][7]) continue;
     int slot, go, soff;
     R::map(row - gg * R::RPS, slot, go, soff);
-    if (p.atomic) row_red<N>(p.x + s_cell[gg][slot] + go, sm + gg * L::SZ + soff, p.omega);
-    else if (coherent) row_update_cg<N>(p.x + s_cell[gg][slot] + go, sm + gg * L::SZ + soff, p.omega);
-    else row_update<N>(p.x + s_cell[gg][slot] + go, sm + gg * L::SZ + soff, p.omega, false);
+    if (p.atomic) row_red<N>(p.x + s_cell[gg][slot] + go, sm + gg * GSZ + soff, p.omega);
+    else if (coherent) row_update_cg<N>(p.x + s_cell[gg][slot] + go, sm + gg * GSZ + soff, p.omega);
+    else row_update<N>(p.x + s_cell[gg][slot] + go, sm + gg * GSZ + soff, p.omega, false);
   }
 }
 
@@ -750,7 +774,7 @@ cluster_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
 
 template <int D, int M>
 __host__ __device__ constexpr int fdm2_smem_doubles() {
-  return fdm2_groups<D, M>() * Lay<D, M>::SZ;
+  return fdm2_groups<D, M>() * fdm_gstride<D, M, fdm2_groups<D, M>()>();
 }
 
 }  // namespace dgb

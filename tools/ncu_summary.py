@@ -18,7 +18,13 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
         "lts__t_bytes.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__instruction_throughput.avg.pct_of_peak_sustained_active",
-        "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second"]
+        "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_lsu_wavefronts.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+        "smsp__inst_executed_op_global_ld.sum", "smsp__inst_executed_op_global_st.sum",
+        "sm__warps_active.avg.per_cycle_active"]
 
 
 def main(path):
