@@ -60,7 +60,7 @@ struct FlowShape {
   static constexpr int GP = fdm2_groups<D, M>();
   static constexpr int NT = GP * Lay<D, M>::F;
   static constexpr int GR = NT / Lay<D, N>::F;  // cells per residual unit
-  static constexpr int SMEM_R = 3 * GR * Lay<D, N>::SZ;
+  static constexpr int SMEM_R = res_smem_doubles<D, N, GR>();
   static constexpr int SMEM_P = GP * fdm_gstride<D, M, GP>();
   static constexpr int SMEM = SMEM_R > SMEM_P ? SMEM_R : SMEM_P;
   // keep the merged residual + patch code at the register budget of the

@@ -28,6 +28,8 @@ static int launch_flow(const ResArgs& ra, const FdmArgs& fa, const HostRes& h, c
   r.start = 0;
   r.count = 0;
   r.packed = 0;
+  r.blocked = 0;
+  r.bz0 = r.bnz = 0;
   r.alpha = ra.alpha;
   r.beta = ra.beta;
   r.betap = ra.betap;

@@ -33,7 +33,20 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
   std::memcpy(p.mats.bg1, h.bg + N, sizeof(p.mats.bg1));
   p.eo = h.eo != nullptr && N % 2 == 0;
   if (p.eo) std::memcpy(p.mats.eo, h.eo, sizeof(p.mats.eo));
-  const int64_t ngroups = (q.count + G - 1) / G;
+  int64_t ngroups = (q.count + G - 1) / G;
+  p.blocked = 0;
+  p.bz0 = p.bnz = 0;
+  if constexpr (D == 3 && G == 8) {
+    // whole layers on 2x2x2 cell blocks: half the neighbour traces come from
+    // the block's own shared tensors
+    const int64_t lc = (int64_t)q.geo.nc[0] * q.geo.nc[1];
+    if (!q.list && q.start % lc == 0 && q.count % lc == 0 && env_int("DGB_RES_BLOCK", 1)) {
+      p.blocked = 1;
+      p.bz0 = q.geo.zb + (int)(q.start / lc);
+      p.bnz = (int)(q.count / lc);
+      ngroups = (int64_t)((q.geo.nc[0] + 1) / 2) * ((q.geo.nc[1] + 1) / 2) * ((p.bnz + 1) / 2);
+    }
+  }
   const size_t smem = sizeof(double) * res2_smem_doubles<D, N>();
   auto k = res2_kernel<D, N>;
   static bool attr = false;

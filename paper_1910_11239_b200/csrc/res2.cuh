@@ -43,8 +43,30 @@ struct Res2Params {
   double alpha, beta, betap;
   int packed;   // list entries are packed global cell coordinates (pack3)
   int eo;       // mass and interior stiffness on the even/odd path
+  int blocked;  // range mode on 2x2x2 cell blocks (G = 8): layers [bz0, bz0 + bnz)
+  int bz0, bnz;
   Geo geo;
   ResMats<N> mats;
+};
+
+// Shared tensor layout of the residual (the padded Lay) and the thread ->
+// (cell, fiber) map per contraction direction.  (Interleaving the cells of a
+// CTA across consecutive threads makes all three directions bank-conflict
+// free but scatters the neighbour-trace loads and row stores over 8 cells;
+// measured slower.)
+template <int D, int N, int G>
+struct RLay {
+  using L = Lay<D, N>;
+  static constexpr int F = L::F;
+  static constexpr int GS = L::SZ;
+  __device__ __forceinline__ static int sstride(int t) { return L::sstride(t); }
+  __device__ __forceinline__ static int sbase(int t, int f) { return L::sbase(t, f); }
+  // shared offset of cell row w (direction-0 fiber w = i1 + n i2)
+  __device__ __forceinline__ static int row(int w) { return L::sbase(0, w); }
+  __device__ __forceinline__ static void who(int, int tid, int& g, int& f) {
+    g = tid / F;
+    f = tid - g * F;
+  }
 };
 
 // cell of work item idx: local id (or -1) and global multi-index
@@ -73,21 +95,32 @@ __device__ __forceinline__ int res_cell(const Geo& geo, const int32_t* list, int
 // neighbour fibers are reduced to their face value and normal derivative
 // before the own fiber is loaded, so at most one fiber-sized array of
 // neighbour data is live (register budget at n = 16).
-template <int D, int N>
+template <int D, int N, class LY>
 __device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, int f,
-                                             const int* c, const double* X, double* out) {
+                                             const int* c, const double* X, double* out,
+                                             const double* XR = nullptr,
+                                             const double* XL = nullptr) {
   using L = Lay<D, N>;
-  const int sb = L::sbase(t, f), ss = L::sstride(t);
+  const int sb = LY::sbase(t, f), ss = LY::sstride(t);
   const int digit = (c[t] == 0 ? 1 : 0) | (c[t] == p.geo.nc[t] - 1 ? 2 : 0);
   const int gb = L::gbase(t, f), gs = L::gstride(t);
   int nb[3] = {c[0], c[1], D == 3 ? c[2] : 0};
   double r_hi = 0.0, r_all = 0.0, l_lo = 0.0, l_all = 0.0;
   if (!(digit & 2)) {  // a_pm x_R: value and normal derivative at the shared face
-    nb[t] = c[t] + 1;
-    const double* q = p.x + (int64_t)cell_local<D>(p.geo, nb) * L::NE + gb;
     double xr[N];
+    if (XR) {  // neighbour tensor of the same CTA block (shared memory)
 #pragma unroll
-    for (int k = 0; k < N; ++k) xr[k] = __ldg(q + k * gs);
+      for (int k = 0; k < N; ++k) xr[k] = XR[sb + k * ss];
+    } else {
+      nb[t] = c[t] + 1;
+      const double* q = p.x + (int64_t)cell_local<D>(p.geo, nb) * L::NE + gb;
+      if (t == 0) {
+        row_load_reg<N>(xr, q);  // a cell row: 16-byte loads for even n
+      } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) xr[k] = __ldg(q + k * gs);
+      }
+    }
     double g = 0.0;
 #pragma unroll
     for (int k = 0; k < N; ++k) g = fma(p.mats.bg0[k], xr[k], g);
@@ -95,11 +128,20 @@ __device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, i
     r_hi = p.alpha * xr[0] + p.beta * g;
   }
   if (!(digit & 1)) {  // a_pm^T x_L
-    nb[t] = c[t] - 1;
-    const double* q = p.x + (int64_t)cell_local<D>(p.geo, nb) * L::NE + gb;
     double xl[N];
+    if (XL) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) xl[k] = __ldg(q + k * gs);
+      for (int k = 0; k < N; ++k) xl[k] = XL[sb + k * ss];
+    } else {
+      nb[t] = c[t] - 1;
+      const double* q = p.x + (int64_t)cell_local<D>(p.geo, nb) * L::NE + gb;
+      if (t == 0) {
+        row_load_reg<N>(xl, q);
+      } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) xl[k] = __ldg(q + k * gs);
+      }
+    }
     double g = 0.0;
 #pragma unroll
     for (int k = 0; k < N; ++k) g = fma(p.mats.bg1[k], xl[k], g);
@@ -142,11 +184,10 @@ __device__ __forceinline__ void res_mass(const Res2Params<D, N>& p, const double
 }
 
 // buf <- M buf along t (in place), optionally adding `add` first
-template <int D, int N, bool ADD>
+template <int D, int N, bool ADD, class LY>
 __device__ __forceinline__ void mass_fiber(const Res2Params<D, N>& p, int t, int f, double* buf,
                                            const double* add) {
-  using L = Lay<D, N>;
-  const int sb = L::sbase(t, f), ss = L::sstride(t);
+  const int sb = LY::sbase(t, f), ss = LY::sstride(t);
   double v[N], o[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) v[k] = ADD ? buf[sb + k * ss] + add[sb + k * ss] : buf[sb + k * ss];
@@ -156,7 +197,7 @@ __device__ __forceinline__ void mass_fiber(const Res2Params<D, N>& p, int t, int
 }
 
 // one group of G cells (work items grp*G .. grp*G+G-1 of the list/range);
-// all NT = G*F threads of the CTA take part; `sm` holds 3*G*SZ doubles.
+// all NT = G*F threads of the CTA take part; `sm` holds res_smem_doubles doubles.
 template <int D, int N, int G>
 __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32_t* list,
                                           int packed, int64_t start, int64_t count, int64_t grp,
@@ -167,71 +208,101 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
   __shared__ int s_cell[G];
   __shared__ int s_c[G][3];
   const int tid = threadIdx.x;
-  if (tid < G) s_cell[tid] = res_cell<D>(p.geo, list, packed, start, count, grp * G + tid, s_c[tid]);
+  constexpr bool BLK = (D == 3 && G == 8);
+  const bool blocked = BLK && p.blocked && !list;
+  if (tid < G) {
+    if (blocked) {
+      // CTA = 2x2x2 cell block; group g = dx + 2 dy + 4 dz
+      const int nbx = (p.geo.nc[0] + 1) >> 1, nby = (p.geo.nc[1] + 1) >> 1;
+      const int64_t bxy = (int64_t)nbx * nby;
+      const int bz = (int)(grp / bxy), rem = (int)(grp - bz * bxy);
+      const int by = rem / nbx, bx = rem - by * nbx;
+      int* c = s_c[tid];
+      c[0] = 2 * bx + (tid & 1);
+      c[1] = 2 * by + ((tid >> 1) & 1);
+      c[2] = p.bz0 + 2 * bz + (tid >> 2);
+      const bool in = c[0] < p.geo.nc[0] && c[1] < p.geo.nc[1] && c[2] < p.bz0 + p.bnz;
+      s_cell[tid] = in ? cell_local<D>(p.geo, c) : -1;
+    } else {
+      s_cell[tid] = res_cell<D>(p.geo, list, packed, start, count, grp * G + tid, s_c[tid]);
+    }
+  }
   __syncthreads();
-  using R = Rows<D, N, false>;
-  for (int row = tid; row < G * R::RPS; row += NT) {
-    const int gg = row / R::RPS;
+  using LY = RLay<D, N, G>;
+  constexpr int GS = LY::GS;
+  constexpr int RPC = (D == 3) ? N * N : N;  // rows per cell
+  for (int row = tid; row < G * RPC; row += NT) {
+    const int gg = row / RPC, w = row - gg * RPC;
     const int cell = s_cell[gg];
     if (cell < 0) continue;
-    int slot, goff, soff;
-    R::map(row - gg * R::RPS, slot, goff, soff);
-    row_load<N>(sm + gg * L::SZ + soff, p.x + (int64_t)cell * L::NE + goff);
+    row_load<N>(sm + gg * GS + LY::row(w), p.x + (int64_t)cell * L::NE + w * N);
   }
-  const int g = tid / F, f = tid - (tid / F) * F;
-  const int cell = s_cell[g];
-  const bool active = cell >= 0;
-  const int c[3] = {s_c[g][0], s_c[g][1], s_c[g][2]};
-  double* X = sm + g * L::SZ;
-  double* A = sm + (G + g) * L::SZ;
-  double* B = sm + (2 * G + g) * L::SZ;
+  // thread -> (cell, fiber) per direction
+  int gt[3], ft[3];
+#pragma unroll
+  for (int t = 0; t < D; ++t) LY::who(t, tid, gt[t], ft[t]);
+  auto X = [&](int t) { return sm + gt[t] * GS; };
+  auto A = [&](int t) { return sm + (G + gt[t]) * GS; };
+  auto B = [&](int t) { return sm + (2 * G + gt[t]) * GS; };
+  auto act = [&](int t) { return s_cell[gt[t]] >= 0; };
+  // in-block neighbour tensors along t (blocked mode): right if bit t of g is 0
+  auto nbr = [&](int t, bool right) -> const double* {
+    if (!blocked) return nullptr;
+    const int g = gt[t];
+    const bool hi = (g >> t) & 1;
+    if (right == hi) return nullptr;
+    const int gn = g ^ (1 << t);
+    return s_cell[gn] >= 0 ? sm + gn * GS : nullptr;
+  };
   __syncthreads();
-  if (active) {
-    stiff2_fiber<D, N>(p, 0, f, c, X, A);
-    stiff2_fiber<D, N>(p, 1, f, c, X, B);
-  }
+  if (act(0)) stiff2_fiber<D, N, LY>(p, 0, ft[0], s_c[gt[0]], X(0), A(0), nbr(0, true), nbr(0, false));
+  if (act(1)) stiff2_fiber<D, N, LY>(p, 1, ft[1], s_c[gt[1]], X(1), B(1), nbr(1, true), nbr(1, false));
   __syncthreads();
-  if (active) {
-    mass_fiber<D, N, false>(p, 1, f, A, nullptr);
-    mass_fiber<D, N, false>(p, 0, f, B, nullptr);
-  }
+  if (act(1)) mass_fiber<D, N, false, LY>(p, 1, ft[1], A(1), nullptr);
+  if (act(0)) mass_fiber<D, N, false, LY>(p, 0, ft[0], B(0), nullptr);
   __syncthreads();
-  // each thread's last fiber (t = 0) is exactly cell row f, so the final
+  // each thread's last fiber (t = 0) is a whole cell row, so the final
   // contraction writes r = b - A x straight to global memory; b is
   // prefetched into registers one phase earlier
-  const int64_t gi = (int64_t)(active ? cell : 0) * L::NE + f * N;
+  const int cell0 = s_cell[gt[0]];
+  const int64_t gi = (int64_t)(cell0 >= 0 ? cell0 : 0) * L::NE + ft[0] * N;
   double bv[N];
   if (D == 3) {
-    if (active) {
-      mass_fiber<D, N, true>(p, 2, f, A, B);   // A = M_2 (M_1 G_0 + M_0 G_1)
-      stiff2_fiber<D, N>(p, 2, f, c, X, B);    // B = G_2 (same fibers as above)
+    if (act(2)) {
+      mass_fiber<D, N, true, LY>(p, 2, ft[2], A(2), B(2));  // A = M_2 (M_1 G_0 + M_0 G_1)
+      stiff2_fiber<D, N, LY>(p, 2, ft[2], s_c[gt[2]], X(2), B(2), nbr(2, true),
+                             nbr(2, false));                 // B = G_2
     }
     __syncthreads();
-    if (active && p.b) row_load_reg<N>(bv, p.b + gi);
-    if (active) mass_fiber<D, N, false>(p, 1, f, B, nullptr);
+    if (act(0) && p.b) row_load_reg<N>(bv, p.b + gi);
+    if (act(1)) mass_fiber<D, N, false, LY>(p, 1, ft[1], B(1), nullptr);
     __syncthreads();
-    if (active) {  // r = b - (A + M_0 B), row f
-      const int sb = L::sbase(0, f);
+    if (act(0)) {  // r = b - (A + M_0 B), row ft[0]
+      const int sb = LY::sbase(0, ft[0]);
+      const double* Bs = B(0);
+      const double* As = A(0);
       double v[N], o[N];
 #pragma unroll
-      for (int k = 0; k < N; ++k) v[k] = B[sb + k];
+      for (int k = 0; k < N; ++k) v[k] = Bs[sb + k];
       res_mass<D, N>(p, v, o);
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        const double ax = A[sb + k] + o[k];
+        const double ax = As[sb + k] + o[k];
         o[k] = p.b ? bv[k] - ax : ax;
       }
       row_store<N>(p.r + gi, o);
     }
   } else {
-    if (active && p.b) row_load_reg<N>(bv, p.b + gi);
-    // 2D: A x = M_1 G_0 + M_0 G_1 = A + B, row f
-    if (active) {
-      const int sb = L::sbase(0, f);
+    if (act(0) && p.b) row_load_reg<N>(bv, p.b + gi);
+    // 2D: A x = M_1 G_0 + M_0 G_1 = A + B, row ft[0]
+    if (act(0)) {
+      const int sb = LY::sbase(0, ft[0]);
+      const double* Bs = B(0);
+      const double* As = A(0);
       double o[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        const double ax = A[sb + k] + B[sb + k];
+        const double ax = As[sb + k] + Bs[sb + k];
         o[k] = p.b ? bv[k] - ax : ax;
       }
       row_store<N>(p.r + gi, o);
@@ -247,9 +318,14 @@ res2_kernel(const __grid_constant__ Res2Params<D, N> p) {
 }
 
 
+template <int D, int N, int G>
+__host__ __device__ constexpr int res_smem_doubles() {
+  return 3 * G * RLay<D, N, G>::GS;
+}
+
 template <int D, int N>
 __host__ __device__ constexpr int res2_smem_doubles() {
-  return 3 * fdm2_groups<D, N>() * Lay<D, N>::SZ;
+  return res_smem_doubles<D, N, fdm2_groups<D, N>()>();
 }
 
 }  // namespace dgb
