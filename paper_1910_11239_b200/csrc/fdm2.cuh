@@ -199,6 +199,12 @@ __device__ __forceinline__ void fiber_inplace(const double (&S)[4][M * M], int d
   for (int k = 0; k < M; ++k) buf[base + k * stride] = o[k];
 }
 
+// x + omega * y with two roundings: the same value the fp64 reduction paths
+// (RED.ADD, bulk reduce-add) produce, so every update path is bitwise equal
+__device__ __forceinline__ double xupd(double x, double omega, double y) {
+  return __dadd_rn(x, __dmul_rn(omega, y));
+}
+
 // one row of N doubles: global <-> shared
 template <int N>
 __device__ __forceinline__ void row_load(double* __restrict__ s, const double* __restrict__ g) {
@@ -227,13 +233,13 @@ __device__ __forceinline__ void row_update(double* __restrict__ g, const double*
 #pragma unroll
     for (int i = 0; i < N; i += 2) {
       double2 v = *reinterpret_cast<const double2*>(g + i);
-      v.x = fma(omega, s[i], v.x);
-      v.y = fma(omega, s[i + 1], v.y);
+      v.x = xupd(v.x, omega, s[i]);
+      v.y = xupd(v.y, omega, s[i + 1]);
       *reinterpret_cast<double2*>(g + i) = v;
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < N; ++i) g[i] = fma(omega, s[i], g[i]);
+    for (int i = 0; i < N; ++i) g[i] = xupd(g[i], omega, s[i]);
   }
 }
 
@@ -261,13 +267,13 @@ __device__ __forceinline__ void row_update_cg(double* __restrict__ g, const doub
 #pragma unroll
     for (int i = 0; i < N; i += 2) {
       double2 v = __ldcg(reinterpret_cast<const double2*>(g + i));
-      v.x = fma(omega, s[i], v.x);
-      v.y = fma(omega, s[i + 1], v.y);
+      v.x = xupd(v.x, omega, s[i]);
+      v.y = xupd(v.y, omega, s[i + 1]);
       __stcg(reinterpret_cast<double2*>(g + i), v);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < N; ++i) __stcg(g + i, fma(omega, s[i], __ldcg(g + i)));
+    for (int i = 0; i < N; ++i) __stcg(g + i, xupd(__ldcg(g + i), omega, s[i]));
   }
 }
 
@@ -361,8 +367,8 @@ __device__ __forceinline__ void reg_update(double* __restrict__ g, const double 
     for (int i = 0; i < N; i += 2) {
       double2 t = coherent ? __ldcg(reinterpret_cast<const double2*>(g + i))
                            : *reinterpret_cast<const double2*>(g + i);
-      t.x = fma(omega, o[h * N + i], t.x);
-      t.y = fma(omega, o[h * N + i + 1], t.y);
+      t.x = xupd(t.x, omega, o[h * N + i]);
+      t.y = xupd(t.y, omega, o[h * N + i + 1]);
       if (coherent) __stcg(reinterpret_cast<double2*>(g + i), t);
       else *reinterpret_cast<double2*>(g + i) = t;
     }
@@ -370,8 +376,8 @@ __device__ __forceinline__ void reg_update(double* __restrict__ g, const double 
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       const double t = coherent ? __ldcg(g + i) : g[i];
-      if (coherent) __stcg(g + i, fma(omega, o[h * N + i], t));
-      else g[i] = fma(omega, o[h * N + i], t);
+      if (coherent) __stcg(g + i, xupd(t, omega, o[h * N + i]));
+      else g[i] = xupd(t, omega, o[h * N + i]);
     }
   }
 }
@@ -395,6 +401,45 @@ struct Rows {
   }
 };
 
+// bulk copies through the TMA engine (no LSU wavefronts on the SM):
+// global -> shared completing on an mbarrier, and shared -> global fp64
+// reduce-add tracked by a bulk group
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, unsigned bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_red_add(double* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(
+                   gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+
 template <int D, int G>
 __host__ __device__ constexpr bool fdm_interleave() {
   return D == 3 && G > 1 && 16 % G == 0;
@@ -413,7 +458,7 @@ __host__ __device__ constexpr int fdm_gstride() {
 // one group of G subdomains (work items grp*G .. grp*G+G-1); all G*F threads
 // of the CTA take part; `sm` holds G*fdm_gstride doubles.  `coherent` reads r and x
 // through L2 only (ld.cg) for use inside a kernel where other CTAs write them.
-template <int D, int M, bool PATCH, int G>
+template <int D, int M, bool PATCH, int G, bool BULK = false>
 __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32_t* list,
                                           int packed, int64_t start, int64_t count, int64_t grp,
                                           double* sm, bool coherent, int delta = -1) {
@@ -470,7 +515,47 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
   constexpr int H = PATCH ? 2 : 1;  // cell rows per direction-0 fiber
   int slot0 = 0, goff = 0;
   fiber_rows<D, M, PATCH>(f, slot0, goff);
-  if (p.direct) {
+  // bulk mode: the cells of R_j r arrive densely (cell-major) in the tensor
+  // buffers by TMA bulk copies, and omega * R_j^T y leaves by bulk fp64
+  // reduce-add; the SM's load/store pipe only sees shared memory
+  // (caller guarantees: NEc even, not coherent, not atomic, no cluster delta)
+  __shared__ __align__(8) uint64_t s_bar;
+  if constexpr (BULK) {
+    if (tid == 0) {
+      mbar_init(&s_bar, 1);
+      unsigned bytes = 0;
+      for (int gg = 0; gg < G; ++gg)
+        if (s_info[gg][7]) bytes += R::SLOTS * NEc * 8;
+      mbar_expect_tx(&s_bar, bytes);
+      for (int gg = 0; gg < G; ++gg)
+        if (s_info[gg][7])
+          for (int sl = 0; sl < R::SLOTS; ++sl)
+            bulk_load(sm + gg * GSZ + sl * NEc, p.r + s_cell[gg][sl], NEc * 8, &s_bar);
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(&s_bar, 0);
+    double v[M], o[M];
+    if (active) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const double* src = buf + (slot0 + h) * NEc + goff;
+#pragma unroll
+        for (int i = 0; i < N; i += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(src + i);
+          v[h * N + i] = t.x;
+          v[h * N + i + 1] = t.y;
+        }
+      }
+      fdm_matvec<M, true>(p.mats, p.eo, dg[0], v, o);
+    }
+    __syncthreads();  // all dense rows read before the padded tensor overwrites them
+    if (active) {
+      const int sb = L::sbase(0, f);
+#pragma unroll
+      for (int k = 0; k < M; ++k) buf[sb + k] = o[k];
+    }
+    __syncthreads();
+  } else if (p.direct) {
     // first forward contraction (direction 0) straight from the global rows of R_j r
     if (active) {
       double v[M], o[M];
@@ -533,6 +618,39 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     if (active) fdm_fiber<M, false>(p.mats, p.eo, dg[t], buf, L::sbase(t, f), L::sstride(t));
     __syncthreads();
   }
+  if constexpr (BULK) {
+    // last backward contraction (direction 0); omega * y rows written densely
+    // over the tensor, then reduce-added into x by the TMA engine
+    double v[M], o[M];
+    if (active) {
+      const int sb = L::sbase(0, f);
+#pragma unroll
+      for (int k = 0; k < M; ++k) v[k] = buf[sb + k];
+      fdm_matvec<M, false>(p.mats, p.eo, dg[0], v, o);
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        double* dst = buf + (slot0 + h) * NEc + goff;
+#pragma unroll
+        for (int i = 0; i < N; i += 2)
+          *reinterpret_cast<double2*>(dst + i) =
+              make_double2(__dmul_rn(p.omega, o[h * N + i]), __dmul_rn(p.omega, o[h * N + i + 1]));
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      for (int gg = 0; gg < G; ++gg)
+        if (s_info[gg][7])
+          for (int sl = 0; sl < R::SLOTS; ++sl)
+            bulk_red_add(p.x + s_cell[gg][sl], sm + gg * GSZ + sl * NEc, NEc * 8);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    return;
+  }
   if (p.direct) {
     // last backward contraction (direction 0) and x += omega R_j^T y from registers
     if (active) {
@@ -561,12 +679,21 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
   }
 }
 
-template <int D, int M, bool PATCH>
-__global__ void __launch_bounds__(fdm2_groups<D, M>() * Lay<D, M>::F)
+// bulk variant: register budget of 56 per thread (4 CTAs of 288 threads per SM)
+template <int D, int M>
+__host__ __device__ constexpr int fdm2_min_ctas(bool bulk) {
+  return bulk ? (65536 / (fdm2_groups<D, M>() * Lay<D, M>::F * 56) > 0
+                     ? 65536 / (fdm2_groups<D, M>() * Lay<D, M>::F * 56)
+                     : 1)
+              : 0;  // 0: no minimum (ptxas default heuristics)
+}
+
+template <int D, int M, bool PATCH, bool BULK = false>
+__global__ void __launch_bounds__(fdm2_groups<D, M>() * Lay<D, M>::F, fdm2_min_ctas<D, M>(BULK))
 fdm2_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
-  extern __shared__ double sm[];
-  fdm_group<D, M, PATCH, fdm2_groups<D, M>()>(p, p.list, p.packed, p.start, p.count, blockIdx.x,
-                                              sm, false);
+  extern __shared__ __align__(16) double sm[];
+  fdm_group<D, M, PATCH, fdm2_groups<D, M>(), BULK>(p, p.list, p.packed, p.start, p.count,
+                                                    blockIdx.x, sm, false);
 }
 
 // fdm6: persistent variant of fdm2 with staggered starts.  All CTAs of a
@@ -578,7 +705,7 @@ template <int D, int M, bool PATCH>
 __global__ void __launch_bounds__(fdm2_groups<D, M>() * Lay<D, M>::F)
 fdm6_kernel(const __grid_constant__ Fdm2Params<D, M> p, int64_t ngroups, int stagger_ns,
             int nsm) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   if (stagger_ns > 0) {
     const int slot = (int)(blockIdx.x / nsm);
     for (int i = 0; i < slot; ++i) __nanosleep(stagger_ns);
@@ -623,7 +750,7 @@ fdm5_kernel(const __grid_constant__ Fdm2Params<D, M> p, int64_t ngroups) {
   using R = Rows<D, M, PATCH>;
   using S = Fdm5Shape<D, M, PATCH>;
   constexpr int N = S::N, G = S::G, F = L::F, NT = S::NT;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   double* Xs = sm + 2 * G * S::SZ;
   __shared__ int s_info[2][G][8];            // digit[3], cls, active
   __shared__ int64_t s_cell[2][G][R::SLOTS];  // dof offset of each cell
@@ -747,7 +874,7 @@ fdm5_kernel(const __grid_constant__ Fdm2Params<D, M> p, int64_t ngroups) {
       const double* xs = Xs + gg * S::XSZ + slot * S::NEc + goff;
       double v[N];
 #pragma unroll
-      for (int i = 0; i < N; ++i) v[i] = fma(p.omega, y[i], xs[i]);
+      for (int i = 0; i < N; ++i) v[i] = xupd(xs[i], p.omega, y[i]);
       row_store<N>(p.x + s_cell[st][gg][slot] + goff, v);
     }
     __syncthreads();  // X and this stage's buffers are refilled next
@@ -763,7 +890,7 @@ fdm5_kernel(const __grid_constant__ Fdm2Params<D, M> p, int64_t ngroups) {
 template <int D, int M>
 __global__ void __launch_bounds__(fdm2_groups<D, M>() * Lay<D, M>::F)
 cluster_kernel(const __grid_constant__ Fdm2Params<D, M> p) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
 #pragma unroll 1
   for (int delta = 0; delta < (1 << D); ++delta) {
     fdm_group<D, M, true, fdm2_groups<D, M>()>(p, p.list, 1, 0, p.count, blockIdx.x, sm, false,

@@ -81,7 +81,7 @@ template <int D, int N>
 __global__ void __launch_bounds__(FlowShape<D, N>::NT, FlowShape<D, N>::MIN_CTAS)
 flow_kernel(const __grid_constant__ FlowParams<D, N> p) {
   using S = FlowShape<D, N>;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   __shared__ int s_task, s_unit;
   const int nt = p.ntasks;
   int* st = p.state;

@@ -33,7 +33,7 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
   if (p.eo) std::memcpy(p.mats.eo, heo, sizeof(p.mats.eo));
   p.pv_lo = q.pv_lo;
   p.pv_hi = q.pv_hi;
-  p.direct = env_int("DGB_DIRECT", 1);
+  p.direct = env_int("DGB_DIRECT", 2);
   if constexpr (D == 3 && M % 8 == 0) {
     // fp64 tensor cores (fdm_mma.cuh) for m = 8, 16
     if (!q.cluster && q.zd && q.ztd && env_int("DGB_MMA", 0)) {
@@ -92,6 +92,19 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
         p, ngroups, env_int("DGB_STAGGER", 2000), nsm);
     DG_CUDA(cudaGetLastError());
     return DG_OK;
+  }
+  if constexpr ((Rows<D, M, PATCH>::N % 2) == 0) {
+    if (p.direct == 2 && !q.atomic && !q.cluster) {
+      auto kb = fdm2_kernel<D, M, PATCH, true>;
+      static bool attr_b = false;
+      if (!attr_b) {
+        DG_CUDA(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_b = true;
+      }
+      kb<<<(unsigned)ngroups, G * Lay<D, M>::F, smem, st>>>(p);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
   }
   auto k = fdm2_kernel<D, M, PATCH>;
   static bool attr = false;

@@ -313,7 +313,7 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
 template <int D, int N>
 __global__ void __launch_bounds__(fdm2_groups<D, N>() * Lay<D, N>::F)
 res2_kernel(const __grid_constant__ Res2Params<D, N> p) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   res_group<D, N, fdm2_groups<D, N>()>(p, p.list, p.packed, p.start, p.count, blockIdx.x, sm);
 }
 
