@@ -1,6 +1,7 @@
 // launch_res.cu - residual kernels (res2.cuh), all (dim, n) instantiations.
 #include "launch.h"
 #include "res2.cuh"
+#include "res3.cuh"
 
 #include <algorithm>
 #include <cstring>
@@ -33,6 +34,28 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
   std::memcpy(p.mats.bg1, h.bg + N, sizeof(p.mats.bg1));
   p.eo = h.eo != nullptr && N % 2 == 0;
   if (p.eo) std::memcpy(p.mats.eo, h.eo, sizeof(p.mats.eo));
+  if constexpr (D == 3 && N >= 7 && N <= 8) {
+    // three-pass residual (res3.cuh); measured faster than res2 for n = 7, 8
+    // only (n = 6: 0.73 vs 0.70 ms on cfg 5)
+    if (env_int("DGB_RES3", 1)) {
+      using S = Res3Shape<N>;
+      const size_t smem3 = sizeof(double) * S::SMEM;
+      const unsigned grid = (unsigned)((q.count + S::G - 1) / S::G);
+      const int minb = env_int("DGB_RES3_MINB", S::MINB);
+      auto k3 = minb >= 3 ? res3_kernel<N, 3> : res3_kernel<N, 2>;
+      static bool attr3 = false;
+      if (!attr3) {
+        DG_CUDA(cudaFuncSetAttribute(res3_kernel<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem3));
+        DG_CUDA(cudaFuncSetAttribute(res3_kernel<N, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem3));
+        attr3 = true;
+      }
+      k3<<<grid, S::NT, smem3, st>>>(p);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
+  }
   int64_t ngroups = (q.count + G - 1) / G;
   p.blocked = 0;
   p.bz0 = p.bnz = 0;

@@ -1,0 +1,252 @@
+// res3.cuh - SIPG residual r = b - A x in 3D with three contraction passes.
+//
+// Same operator as res2.cuh (dgop.py:762-788, Kronecker-sum form of SURVEY
+// App. A.5), regrouped so that every pass reads each tensor once:
+//   a = G_0 x,   b = M_0 x                       (pass t = 0, row in registers)
+//   c = M_1 a + G_1 b,   d = M_1 b               (pass t = 1, in place)
+//   A x = M_2 c + G_2 d                          (pass t = 2, written to global)
+// = M_2 M_1 G_0 x + M_2 G_1 M_0 x + G_2 M_1 M_0 x.
+// G_1 and G_2 act on mass-transformed data, so their face couplings need the
+// neighbour traces transformed the same way: the four face scalars per
+// transverse position (R_all = beta' x_R[0], R_hi = alpha x_R[0] + beta bg0.x_R,
+// L_all = beta x_L[n-1], L_lo = alpha x_L[n-1] + beta' bg1.x_L) are computed
+// raw into small 2D fields and the transverse masses are applied to those
+// fields (2D work, n^2 per field).  Shared traffic per cell: 8 tensor
+// accesses per DoF (res2: 18), 7 tensor contractions (res2: 8).
+#pragma once
+#include "res2.cuh"
+
+namespace dgb {
+
+template <int N>
+struct Res3Shape {
+  using L = Lay<3, N>;
+  static constexpr int G = fdm2_groups<3, N>();
+  static constexpr int F = N * N;
+  static constexpr int NT = G * F;
+  static constexpr int CS = 2 * L::SZ + 8 * N * N;  // A, B tensors + F1[4], F2[4] fields
+  static constexpr int SMEM = G * CS;                // doubles
+  // CTAs per SM the register budget is sized for (launch_res.cu: DGB_RES3_MINB)
+  static constexpr int MINB = 2;
+};
+
+// the four face scalars of a fiber along t (zero where the neighbour is absent)
+template <int N>
+__device__ __forceinline__ void face_scalars(const Res2Params<3, N>& p, const double* xr,
+                                             const double* xl, int gs, double (&fq)[4]) {
+  fq[0] = fq[1] = fq[2] = fq[3] = 0.0;
+  if (xr) {
+    double v[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = __ldg(xr + k * gs);
+    double g = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) g = fma(p.mats.bg0[k], v[k], g);
+    fq[0] = p.betap * v[0];
+    fq[1] = p.alpha * v[0] + p.beta * g;
+  }
+  asm volatile("" ::: "memory");  // one neighbour fiber live at a time (registers)
+  if (xl) {
+    double v[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = __ldg(xl + k * gs);
+    double g = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) g = fma(p.mats.bg1[k], v[k], g);
+    fq[2] = p.beta * v[N - 1];
+    fq[3] = p.alpha * v[N - 1] + p.betap * g;
+  }
+}
+
+// o += face couplings of the four scalars along the fiber
+template <int N>
+__device__ __forceinline__ void add_faces(const Res2Params<3, N>& p, const double (&fq)[4],
+                                          double (&o)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) o[i] = fma(p.mats.bg1[i], fq[0], fma(p.mats.bg0[i], fq[2], o[i]));
+  o[N - 1] += fq[1];
+  o[0] += fq[3];
+}
+
+template <int N>
+__device__ __forceinline__ void res_adiag(const Res2Params<3, N>& p, int digit,
+                                          const double (&v)[N], double (&o)[N]) {
+  if constexpr (N % 2 == 0) {
+    if (p.eo && digit == 0) {
+      matvec_cs<N>(p.mats.eo[2], p.mats.eo[3], v, o);
+      return;
+    }
+  }
+  matvec_digit<N>(p.mats.adiag, digit, v, o);
+}
+
+template <int N>
+__device__ __forceinline__ void mass3(const Res2Params<3, N>& p, const double (&v)[N],
+                                      double (&o)[N]) {
+  res_mass<3, N>(p, v, o);
+}
+
+template <int N, int MINB>
+__global__ void __launch_bounds__(Res3Shape<N>::NT, MINB)
+res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
+  using S = Res3Shape<N>;
+  using L = Lay<3, N>;
+  constexpr int G = S::G, F = S::F, NE = L::NE;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_cell[G];
+  __shared__ int s_c[G][3];
+  const int tid = threadIdx.x;
+  if (tid < G)
+    s_cell[tid] = res_cell<3>(p.geo, p.list, p.packed, p.start, p.count,
+                              (int64_t)blockIdx.x * G + tid, s_c[tid]);
+  __syncthreads();
+  const int g = tid / F, f = tid - g * F;
+  const int cell = s_cell[g];
+  const bool active = cell >= 0;
+  int c[3] = {s_c[g][0], s_c[g][1], s_c[g][2]};
+  int dig[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) dig[t] = (c[t] == 0 ? 1 : 0) | (c[t] == p.geo.nc[t] - 1 ? 2 : 0);
+  double* A = sm + g * S::CS;
+  double* B = A + L::SZ;
+  double* F1 = B + L::SZ;      // F1[q][i2][i0]: faces along t = 1
+  double* F2 = F1 + 4 * F;     // F2[q][i1][i0]: faces along t = 2
+  const int fa = f % N, fb = f / N;
+  const int64_t cb = (int64_t)(active ? cell : 0) * NE;
+  auto nbr = [&](int t, int dir) -> const double* {  // neighbour cell data or null
+    if (dir > 0 ? (dig[t] & 2) : (dig[t] & 1)) return nullptr;
+    int nb[3] = {c[0], c[1], c[2]};
+    nb[t] += dir;
+    return p.x + (int64_t)cell_local<3>(p.geo, nb) * NE;
+  };
+  // ---- pass t = 0: own row (i1, i2) = (fa, fb) from global; raw face fields
+  if (active) {
+    double v[N], o[N];
+    row_load_reg<N>(v, p.x + cb + f * N);
+    double fq[4] = {0.0, 0.0, 0.0, 0.0};
+    {
+      const double* r = nbr(0, +1);
+      const double* l = nbr(0, -1);
+      if (r) {
+        double w[N];
+        row_load_reg<N>(w, r + f * N);
+        double gg = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) gg = fma(p.mats.bg0[k], w[k], gg);
+        fq[0] = p.betap * w[0];
+        fq[1] = p.alpha * w[0] + p.beta * gg;
+      }
+      asm volatile("" ::: "memory");
+      if (l) {
+        double w[N];
+        row_load_reg<N>(w, l + f * N);
+        double gg = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) gg = fma(p.mats.bg1[k], w[k], gg);
+        fq[2] = p.beta * w[N - 1];
+        fq[3] = p.alpha * w[N - 1] + p.betap * gg;
+      }
+    }
+    res_adiag<N>(p, dig[0], v, o);
+    add_faces<N>(p, fq, o);
+    const int sb = L::sbase(0, f);
+#pragma unroll
+    for (int k = 0; k < N; ++k) A[sb + k] = o[k];
+    mass3<N>(p, v, o);
+#pragma unroll
+    for (int k = 0; k < N; ++k) B[sb + k] = o[k];
+    asm volatile("" ::: "memory");
+    // faces along t = 1 at (i0, i2) = (fa, fb): fibers stride n
+    {
+      const double* r = nbr(1, +1);
+      const double* l = nbr(1, -1);
+      const int gb = fa + N * N * fb;
+      face_scalars<N>(p, r ? r + gb : nullptr, l ? l + gb : nullptr, N, fq);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) F1[q * F + fb * N + fa] = fq[q];
+    }
+    asm volatile("" ::: "memory");
+    // faces along t = 2 at (i0, i1) = (fa, fb): fibers stride n^2
+    {
+      const double* r = nbr(2, +1);
+      const double* l = nbr(2, -1);
+      const int gb = fa + N * fb;
+      face_scalars<N>(p, r ? r + gb : nullptr, l ? l + gb : nullptr, N * N, fq);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) F2[q * F + fb * N + fa] = fq[q];
+    }
+  }
+  __syncthreads();
+  // ---- M_0 along i0 of the face fields, rows F1[q][i2][.] and F2[q][i1][.]
+  if (active) {
+    for (int w = f; w < 8 * N; w += F) {  // in place, one thread per row
+      double* row = F1 + (w / N) * F + (w % N) * N;
+      double v[N], o[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = row[j];
+      mass3<N>(p, v, o);
+#pragma unroll
+      for (int j = 0; j < N; ++j) row[j] = o[j];
+    }
+  }
+  __syncthreads();
+  // ---- pass t = 1 at (i0, i2) = (fa, fb); M_1 along i1 of the F2 columns
+  double bq[N];
+  if (active) {
+    for (int w = f; w < 4 * N; w += F) {  // F2 column (q, i0): in place
+      double* col = F2 + (w / N) * F + (w % N);
+      double v[N], o[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = col[j * N];
+      mass3<N>(p, v, o);
+#pragma unroll
+      for (int j = 0; j < N; ++j) col[j * N] = o[j];
+    }
+    const int sb = L::sbase(1, f), ss = L::sstride(1);
+    double v[N], o[N], t[N];
+    double fq[4];  // faces along t = 1, transformed by M_0
+#pragma unroll
+    for (int q = 0; q < 4; ++q) fq[q] = F1[q * F + fb * N + fa];
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = B[sb + k * ss];
+    res_adiag<N>(p, dig[1], v, t);  // G_1 b
+    add_faces<N>(p, fq, t);
+    mass3<N>(p, v, o);        // d = M_1 b
+#pragma unroll
+    for (int k = 0; k < N; ++k) B[sb + k * ss] = o[k];
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = A[sb + k * ss];
+    mass3<N>(p, v, o);        // c = M_1 a + G_1 b
+#pragma unroll
+    for (int k = 0; k < N; ++k) A[sb + k * ss] = o[k] + t[k];
+    // right-hand side along the t = 2 fiber (i0, i1) = (fa, fb)
+    if (p.b) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) bq[k] = __ldg(p.b + cb + fa + N * fb + N * N * k);
+    }
+  }
+  __syncthreads();
+  // ---- pass t = 2 at (i0, i1) = (fa, fb); faces transformed by M_1 along i1
+  if (active) {
+    const int sb = L::sbase(2, f), ss = L::sstride(2);
+    double v[N], o[N], t[N];
+    double fq[4];  // faces along t = 2, transformed by M_0 and M_1
+#pragma unroll
+    for (int q = 0; q < 4; ++q) fq[q] = F2[q * F + fb * N + fa];
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = B[sb + k * ss];
+    res_adiag<N>(p, dig[2], v, t);  // G_2 d
+    add_faces<N>(p, fq, t);
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = A[sb + k * ss];
+    mass3<N>(p, v, o);        // M_2 c
+    double* r = p.r + cb + fa + N * fb;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const double ax = o[k] + t[k];
+      r[N * N * k] = p.b ? bq[k] - ax : ax;
+    }
+  }
+}
+
+}  // namespace dgb

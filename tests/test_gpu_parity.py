@@ -46,7 +46,7 @@ def test_operator_and_residual_match_reference(name):
 
 
 @pytest.mark.parametrize("d,nc,k", [(2, 64, 3), (3, 32, 3), (3, 16, 15), (3, 12, 7),
-                                    (3, 16, 5), (2, 9, 9), (3, 5, 11)])
+                                    (3, 16, 5), (2, 9, 9), (3, 5, 11), (3, 7, 6), (3, 6, 4)])
 def test_operator_matches_oracle_at_size(d, nc, k):
     ctx, _, _ = _setup(d, nc, k)
     x0, b = inputs(ctx.ndofs, 11)
@@ -54,6 +54,21 @@ def test_operator_matches_oracle_at_size(d, nc, k):
     assert rel(dg.apply_operator(ctx, x0), lvl.apply(x0)) <= RTOL
     r = np.empty(ctx.ndofs)
     assert rel(dg.residual(ctx, x0, b, out=r), lvl.residual(x0, b)) <= RTOL
+
+
+@pytest.mark.parametrize("k", [3, 5, 6, 7])
+def test_residual_kernel_variants_agree(k, monkeypatch):
+    """res2 (five passes) and res3 (three passes, mass-transformed face
+    fields) regroup the same sums: equal to rounding, and both at the oracle."""
+    ctx, _, _ = _setup(3, 7, k)
+    x0, b = inputs(ctx.ndofs, 12)
+    want = OracleLevel((7,) * 3, k).residual(x0, b)
+    got = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv("DGB_RES3", v)
+        got[v] = dg.residual(ctx, x0, b, out=np.empty(ctx.ndofs))
+        assert rel(got[v], want) <= RTOL
+    assert rel(got["0"], got["1"]) <= 1e-14
 
 
 def test_operator_symmetric_full_cfg5_size():
@@ -267,6 +282,8 @@ def test_dataflow_avs_kernel_bitwise_equals_colour_launches(d, nc, k, monkeypatc
     monkeypatch.setenv("DGB_CLUSTER", "0")
     monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
     monkeypatch.setenv("DGB_FLOW", "0")
+    # the dataflow kernel's residual tasks run res2's arithmetic
+    monkeypatch.setenv("DGB_RES3", "0")
     xa = x0.copy()
     sm.smooth(xa, b)
     monkeypatch.setenv("DGB_FLOW", "1")
