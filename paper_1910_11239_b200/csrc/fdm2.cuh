@@ -440,6 +440,14 @@ __device__ __forceinline__ void bulk_red_add(double* gdst, const void* ssrc, uns
                : "memory");
 }
 
+// shared offset of cell slot s in the dense (bulk-staged) layout: the small
+// skew keeps the 16-byte row accesses of a quarter-warp that straddles two
+// cells in distinct bank groups (fits: 8 cells + 8 doubles <= tensor size)
+template <int NEc>
+__host__ __device__ constexpr int dense_off(int s) {
+  return s * NEc + 4 * ((s + 2) >> 2);
+}
+
 template <int D, int G>
 __host__ __device__ constexpr bool fdm_interleave() {
   return D == 3 && G > 1 && 16 % G == 0;
@@ -519,6 +527,7 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
   // buffers by TMA bulk copies, and omega * R_j^T y leaves by bulk fp64
   // reduce-add; the SM's load/store pipe only sees shared memory
   // (caller guarantees: NEc even, not coherent, not atomic, no cluster delta)
+  static_assert(!BULK || dense_off<NEc>(R::SLOTS - 1) + NEc <= GSZ, "dense staging fits");
   __shared__ __align__(8) uint64_t s_bar;
   if constexpr (BULK) {
     if (tid == 0) {
@@ -530,7 +539,7 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
       for (int gg = 0; gg < G; ++gg)
         if (s_info[gg][7])
           for (int sl = 0; sl < R::SLOTS; ++sl)
-            bulk_load(sm + gg * GSZ + sl * NEc, p.r + s_cell[gg][sl], NEc * 8, &s_bar);
+            bulk_load(sm + gg * GSZ + dense_off<NEc>(sl), p.r + s_cell[gg][sl], NEc * 8, &s_bar);
     }
     __syncthreads();  // barrier initialised before anyone waits on it
     mbar_wait(&s_bar, 0);
@@ -538,7 +547,7 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     if (active) {
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        const double* src = buf + (slot0 + h) * NEc + goff;
+        const double* src = buf + dense_off<NEc>(slot0 + h) + goff;
 #pragma unroll
         for (int i = 0; i < N; i += 2) {
           const double2 t = *reinterpret_cast<const double2*>(src + i);
@@ -632,7 +641,7 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     if (active) {
 #pragma unroll
       for (int h = 0; h < H; ++h) {
-        double* dst = buf + (slot0 + h) * NEc + goff;
+        double* dst = buf + dense_off<NEc>(slot0 + h) + goff;
 #pragma unroll
         for (int i = 0; i < N; i += 2)
           *reinterpret_cast<double2*>(dst + i) =
@@ -645,7 +654,7 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
       for (int gg = 0; gg < G; ++gg)
         if (s_info[gg][7])
           for (int sl = 0; sl < R::SLOTS; ++sl)
-            bulk_red_add(p.x + s_cell[gg][sl], sm + gg * GSZ + sl * NEc, NEc * 8);
+            bulk_red_add(p.x + s_cell[gg][sl], sm + gg * GSZ + dense_off<NEc>(sl), NEc * 8);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
