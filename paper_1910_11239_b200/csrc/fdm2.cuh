@@ -530,16 +530,22 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
   static_assert(!BULK || dense_off<NEc>(R::SLOTS - 1) + NEc <= GSZ, "dense staging fits");
   __shared__ __align__(8) uint64_t s_bar;
   if constexpr (BULK) {
-    if (tid == 0) {
-      mbar_init(&s_bar, 1);
-      unsigned bytes = 0;
-      for (int gg = 0; gg < G; ++gg)
-        if (s_info[gg][7]) bytes += R::SLOTS * NEc * 8;
-      mbar_expect_tx(&s_bar, bytes);
-      for (int gg = 0; gg < G; ++gg)
+    // warp 0 issues the G * 2^d cell copies in parallel (one per lane); the
+    // single arrival (lane 0's expect_tx) keeps the phase open until all land
+    if (tid < 32) {
+      if (tid == 0) mbar_init(&s_bar, 1);
+      __syncwarp();
+      if (tid == 0) {
+        unsigned bytes = 0;
+        for (int gg = 0; gg < G; ++gg)
+          if (s_info[gg][7]) bytes += R::SLOTS * NEc * 8;
+        mbar_expect_tx(&s_bar, bytes);
+      }
+      for (int l = tid; l < G * R::SLOTS; l += 32) {
+        const int gg = l / R::SLOTS, sl = l - gg * R::SLOTS;
         if (s_info[gg][7])
-          for (int sl = 0; sl < R::SLOTS; ++sl)
-            bulk_load(sm + gg * GSZ + dense_off<NEc>(sl), p.r + s_cell[gg][sl], NEc * 8, &s_bar);
+          bulk_load(sm + gg * GSZ + dense_off<NEc>(sl), p.r + s_cell[gg][sl], NEc * 8, &s_bar);
+      }
     }
     __syncthreads();  // barrier initialised before anyone waits on it
     mbar_wait(&s_bar, 0);
@@ -650,13 +656,19 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (tid == 0) {
-      for (int gg = 0; gg < G; ++gg)
-        if (s_info[gg][7])
-          for (int sl = 0; sl < R::SLOTS; ++sl)
-            bulk_red_add(p.x + s_cell[gg][sl], sm + gg * GSZ + dense_off<NEc>(sl), NEc * 8);
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (tid < 32) {  // one reduce per lane; each lane waits for its own group
+      bool any = false;
+      for (int l = tid; l < G * R::SLOTS; l += 32) {
+        const int gg = l / R::SLOTS, sl = l - gg * R::SLOTS;
+        if (s_info[gg][7]) {
+          bulk_red_add(p.x + s_cell[gg][sl], sm + gg * GSZ + dense_off<NEc>(sl), NEc * 8);
+          any = true;
+        }
+      }
+      if (any) {
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
     }
     return;
   }
