@@ -150,6 +150,33 @@ int64_t dg_last_launch_count(const dg_level_t* lvl);
  * 0 if it runs as one residual launch plus one launch per colour.           */
 int dg_flow_enabled(const dg_level_t* lvl);
 
+
+/* Nested-level transfers between a coarse level with coarse_cells[t] cells
+ * per direction and its uniform refinement (2*coarse_cells[t]); e0, e1 are
+ * the host 1D embeddings E^s[i*n+j] = phi_j((x_i+s)/2) (build_transfer,
+ * multigrid.py:51-55), n = degree+1.  Vectors are device fp64 canonical.
+ * dg_prolongate: xf = P xc, or xf += P xc when accumulate != 0 (the
+ *   V-cycle's coarse-grid correction, multigrid.py:340-341)
+ *   (LevelTransfer.prolongate, multigrid.py:91-108);
+ * dg_restrict:   xc = P^T xf (LevelTransfer.restrict, multigrid.py:110-130). */
+int dg_prolongate(int dim, int degree, const int* coarse_cells, const double* e0,
+                  const double* e1, const double* xc, double* xf, int accumulate,
+                  void* stream);
+int dg_restrict(int dim, int degree, const int* coarse_cells, const double* e0,
+                const double* e1, const double* xf, double* xc, void* stream);
+
+/* Fused vector kernels of the device-resident CG (krylov.pcg,
+ * krylov.py:69-123).  `part` is device scratch of >= 1024 doubles, `out` one
+ * device double receiving the (deterministic, fixed-order) reduction.
+ * dg_cg_update: x += alpha p; r -= alpha ap; *out = r.r
+ * dg_xpby:      p = z + beta p
+ * dg_dot:       *out = a.b                                                 */
+int dg_cg_update(double* x, double* r, const double* p, const double* ap, double alpha,
+                 int64_t n, double* part, double* out, void* stream);
+int dg_xpby(const double* z, double beta, double* p, int64_t n, void* stream);
+int dg_dot(const double* a, const double* b, int64_t n, double* part, double* out,
+           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

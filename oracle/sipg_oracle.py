@@ -16,13 +16,19 @@ as cubes:
 - residual `dgop.py:782-788`;
 - cell / patch fast-diagonalisation solves `fastdiag.py:89-133`, `457-496`,
   `602-628`, index maps `fastdiag.py:546-582`, `mesh.py:297-326`;
-- colourings `mesh.py:350-375`; smoothing steps `smoothers.py:131-166`.
+- colourings `mesh.py:350-375`; smoothing steps `smoothers.py:131-166`;
+- multigrid: 1D embeddings `multigrid.py:51-55`,
+  prolongation / restriction `multigrid.py:91-130`, the V-cycle with a dense
+  coarse solve `multigrid.py:326-350`; preconditioned CG `krylov.py:69-123`.
 
 Parity pin: `tests/test_oracle.py` checks this oracle against golden vectors
-produced by the reference itself (`tests/golden/make_golden.py`).
+produced by the reference itself (`tests/golden/make_golden.py`,
+`tests/golden/make_golden_mg.py`).
 """
 
 from __future__ import annotations
+
+import itertools
 
 import numpy as np
 from numpy.polynomial import legendre as npleg
@@ -326,3 +332,102 @@ def seeded_inputs(ndofs, seed=0):
     b = np.random.default_rng(seed).uniform(-1.0, 1.0, ndofs)
     x0 = np.random.default_rng(seed + 1).uniform(-1.0, 1.0, ndofs)
     return x0, b
+
+
+# ------------------------------------------------- multigrid --
+def embeddings(k):
+    """E^s[i, j] = phi_j((x_i + s) / 2), s = 0, 1 (`multigrid.py:51-55`)."""
+    nodes = gl_nodes(k)
+    return lagrange(nodes, nodes / 2.0)[0].T.copy(), lagrange(nodes, (nodes + 1.0) / 2.0)[0].T.copy()
+
+
+def _children(dims, n):
+    """(child bits s_t per direction, fine-grid slice) for the 2^d children."""
+    d = len(dims)
+    for s in itertools.product((0, 1), repeat=d):
+        sl = [slice(None)] * (2 * d)
+        for t in range(d):
+            sl[d - 1 - t] = slice(s[t], None, 2)   # cell axis of direction t
+        yield s, tuple(sl)
+
+
+def prolongate(dims, k, xc):
+    """Fine cell 2c+s gets (E^{s_d} x .. x E^{s_1}) x_c (`multigrid.py:91-108`);
+    `dims` are the coarse cells per direction."""
+    d, n = len(dims), k + 1
+    e = embeddings(k)
+    X = np.asarray(xc, dtype=float).reshape(tuple(dims[::-1]) + (n,) * d)
+    F = np.empty(tuple(2 * v for v in dims[::-1]) + (n,) * d)
+    for s, sl in _children(dims, n):
+        Y = X
+        for t in range(d):
+            Y = _along(Y, e[s[t]], 2 * d - 1 - t)
+        F[sl] = Y
+    return F.reshape(-1)
+
+
+def restrict(dims, k, xf):
+    """Adjoint of `prolongate` (`multigrid.py:110-130`)."""
+    d, n = len(dims), k + 1
+    e = embeddings(k)
+    F = np.asarray(xf, dtype=float).reshape(tuple(2 * v for v in dims[::-1]) + (n,) * d)
+    X = np.zeros(tuple(dims[::-1]) + (n,) * d)
+    for s, sl in _children(dims, n):
+        Y = F[sl]
+        for t in range(d):
+            Y = _along(Y, e[s[t]].T, 2 * d - 1 - t)
+        X += Y
+    return X.reshape(-1)
+
+
+class OracleVCycle:
+    """V-cycle over cube levels coarse*2^l (`multigrid.py:296-350`) with a
+    dense direct coarse solve (`multigrid.py:170-176`)."""
+
+    def __init__(self, d, coarse, levels, k, kind, omega, m_pre=1, m_post=1,
+                 symmetrize=False):
+        self.levels = [OracleLevel((coarse * 2 ** l,) * d, k) for l in range(levels + 1)]
+        self.k, self.kind, self.omega = k, kind, omega
+        self.m_pre, self.m_post, self.sym = m_pre, m_post, symmetrize
+        self._a0 = self.levels[0].dense()
+
+    def vcycle(self, ell, x, b):
+        if ell == 0:
+            return np.linalg.solve(self._a0, b)
+        lv = self.levels[ell]
+        for _ in range(self.m_pre):
+            x = lv.smooth(self.kind, self.omega, x, b)
+        bc = restrict(self.levels[ell - 1].dims, self.k, lv.residual(x, b))
+        xc = self.vcycle(ell - 1, np.zeros_like(bc), bc)
+        x = x + prolongate(self.levels[ell - 1].dims, self.k, xc)
+        for _ in range(self.m_post):
+            x = lv.smooth(self.kind, self.omega, x, b, reverse=self.sym)
+        return x
+
+    def apply(self, b):
+        return self.vcycle(len(self.levels) - 1, np.zeros_like(b), b)
+
+
+def pcg(apply_op, b, precond, delta_red=1e-8, max_it=200):
+    """Preconditioned CG (`krylov.py:69-123`): returns (x, residual history)."""
+    x = np.zeros_like(b)
+    r = b.copy()
+    hist = [np.linalg.norm(r)]
+    if hist[0] == 0.0:
+        return x, hist
+    z = precond(r)
+    p = z.copy()
+    rz = r @ z
+    for _ in range(max_it):
+        ap = apply_op(p)
+        alpha = rz / (p @ ap)
+        x += alpha * p
+        r -= alpha * ap
+        hist.append(np.linalg.norm(r))
+        if hist[-1] <= delta_red * hist[0]:
+            break
+        z = precond(r)
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x, hist

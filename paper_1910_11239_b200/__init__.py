@@ -6,12 +6,14 @@ the additive / coloured-multiplicative smoothing steps, computed by
 hand-written sm_100a CUDA kernels behind a C ABI (include/dgmg_b200.h).
 """
 
-from . import basis, dgop, fastdiag, flops, mesh, smoothers, tables  # noqa: F401
+from . import basis, dgop, fastdiag, flops, krylov, mesh, multigrid, smoothers, tables  # noqa: F401
 from .basis import Basis1D  # noqa: F401
 from .dgop import apply_operator, make_context, residual  # noqa: F401
 from .fastdiag import CellSolverSet, PatchSolverSet, SingularLocalSolverError  # noqa: F401
 from .flops import FlopCounter  # noqa: F401
+from .krylov import pcg, pgmres  # noqa: F401
 from .mesh import build_hierarchy, box_level  # noqa: F401
+from .multigrid import LevelTransfer, MultigridConfig, VCycle, build_transfer  # noqa: F401
 from .smoothers import (LevelSmoother, SmootherConfig, make_level_smoother,  # noqa: F401
                         smooth_additive, smooth_multiplicative)
 

@@ -20,6 +20,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import numpy as np
+import torch
 
 from . import _lib
 from ._device import Staged, require_cuda, stream_handle
@@ -35,6 +36,7 @@ __all__ = [
     "make_context",
     "apply_operator",
     "residual",
+    "assemble_dense",
 ]
 
 
@@ -193,3 +195,72 @@ def residual(ctx: OperatorContext, x, b, out, kernel: str = "residual"):
     _count_apply(ctx, kernel)
     ctx.count(kernel, ctx.ndofs)
     return out
+
+
+def _coupling(t: LevelTables) -> np.ndarray:
+    """Rank-2 face coupling a_pm = alpha e_n e_1^T + beta e_n bg0^T +
+    betap bg1 e_1^T (`polybasis.py:278-284`; GL end nodes are nodal)."""
+    n = t.n
+    a = np.zeros((n, n))
+    a[n - 1, 0] += t.alpha
+    a[n - 1, :] += t.beta * t.bg[0]
+    a[:, 0] += t.betap * t.bg[1]
+    return a
+
+
+def assemble_dense(ctx: OperatorContext, via: str = "kronecker", device=None):
+    """Dense level matrix in the canonical layout (cf. `dgop.py:1045-1072`),
+    for coarse levels: on a Cartesian level A = sum_t M (x) .. A_g^(t) .. (x) M
+    with block-tridiagonal 1D A_g, permuted from the
+    direction-major to the canonical dof order.  Built with torch on `device`
+    (the 1D factors are host setup); returns a numpy array when device is
+    None.  `via="matvec"` assembles from device operator applications."""
+    lay = ctx.layout
+    ndofs = lay.ndofs
+    if ndofs > 40000:
+        raise ValueError("dense assembly limited to 40000 dofs")
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    if via == "matvec":
+        eye = torch.eye(ndofs, dtype=torch.float64, device="cuda")
+        a = torch.empty((ndofs, ndofs), dtype=torch.float64, device="cuda")
+        for j in range(ndofs):
+            apply_operator(ctx, eye[j], out=a[j])
+        a = a.T.contiguous().to(dev)
+        return a.numpy() if device is None else a
+    if via not in ("kronecker", "quadrature"):
+        raise ValueError("via must be 'kronecker', 'quadrature' or 'matvec'")
+    t = ctx.tables
+    n, d, dims = lay.n1d, lay.dim, lay.dims
+    apm = _coupling(t)
+    ag, mg = [], []
+    for dt in range(d):
+        nt = dims[dt]
+        a1 = np.zeros((nt * n, nt * n))
+        for c in range(nt):
+            digit = (1 if c == 0 else 0) | (2 if c == nt - 1 else 0)
+            a1[c * n:(c + 1) * n, c * n:(c + 1) * n] = t.adiag[digit]
+            if c + 1 < nt:
+                a1[c * n:(c + 1) * n, (c + 1) * n:(c + 2) * n] = apm
+                a1[(c + 1) * n:(c + 2) * n, c * n:(c + 1) * n] = apm.T
+        ag.append(torch.from_numpy(a1).to(dev))
+        mg.append(torch.from_numpy(np.kron(np.eye(nt), t.mass)).to(dev))
+    a = None
+    for dt in range(d):
+        term = None
+        for u in reversed(range(d)):          # kron order: slowest direction first
+            f = ag[u] if u == dt else mg[u]
+            term = f if term is None else torch.kron(term, f)
+        a = term if a is None else a + term
+    # canonical dof g = cell n^d + sum_t i_t n^(t-1) -> direction-major index
+    shape = tuple(dims[::-1]) + (n,) * d
+    idx = np.indices(shape).reshape(2 * d, -1)
+    jdm = np.zeros(idx.shape[1], dtype=np.int64)
+    stride = 1
+    for dt in range(d):
+        c_t = idx[d - 1 - dt]
+        i_t = idx[2 * d - 1 - dt]
+        jdm += (c_t * n + i_t) * stride
+        stride *= dims[dt] * n
+    perm = torch.from_numpy(jdm).to(dev)
+    a = a.index_select(0, perm).index_select(1, perm)
+    return a.numpy() if device is None else a

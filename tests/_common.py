@@ -35,3 +35,19 @@ def rel(a, b):
 
 def have_reference():
     return os.path.isdir(REF_SRC)
+
+
+GOLDEN_MG = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_mg.npz")
+_gold_mg = None
+
+
+def golden_mg():
+    global _gold_mg
+    if _gold_mg is None:
+        _gold_mg = dict(np.load(GOLDEN_MG))
+    return _gold_mg
+
+
+def useed(n, seed):
+    """default_rng(seed).uniform(-1, 1, n) (tests/golden/make_golden_mg.py)."""
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
