@@ -111,6 +111,8 @@ struct dg_level {
   std::vector<DevList> pcol_cells_pk;
   std::vector<DevList> clus_pk;     // AVS clusters per cluster colour, packed base vertices
   DevList pall_pk;                  // all patches (colour order), packed, one-launch AVS
+  std::vector<DevList> pwin_pk;     // AVS launch order: (z-window, parity class), packed
+  int avs_win = 0;                  // z-window of pwin_pk in patch vertices (0 = whole level)
   FlowDev flow;                     // dataflow AVS step (flow.cuh)
   bool flow_ok = false;
   cudaStream_t cap = nullptr;       // capture stream
@@ -130,7 +132,7 @@ static void free_level(dg_level* L) {
   if (!L) return;
   for (auto& kv : L->graphs) cudaGraphExecDestroy(kv.second);
   for (auto* v : {&L->rb, &L->rb_pk, &L->pcol, &L->pcol_pk, &L->pcol_cells, &L->pcol_cells_pk,
-                  &L->clus_pk})
+                  &L->clus_pk, &L->pwin_pk})
     for (auto& l : *v) cudaFree(l.ptr);
   cudaFree(L->pall_pk.ptr);
   cudaFree(L->dtab);
@@ -535,6 +537,37 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
       for (int k = 0; k < ncol; ++k) all.insert(all.end(), pcp[k].begin(), pcp[k].end());
       if (int rc = upload_list(all, &L->pall_pk)) { free_level(L); return rc; }
     }
+    // Additive launch order.  Colours 2q and 2q+1 share the vertex parity q,
+    // so together they are write-disjoint (stride-2 vertex lattice) and one
+    // launch serves both; every dof still receives its parity-class updates
+    // in class order, so with one window this is bitwise the colour-by-colour
+    // step.  With W > 0 the classes run window by window along the last
+    // direction (v_last in [1 + wW, 1 + (w+1)W), global windows), so a
+    // window's x and r (W+1 cell layers) stay in L2 across its 2^d class
+    // launches; only dofs of a window's boundary layer see their updates in
+    // (window, class) order instead (rounding-level difference, identical on
+    // every slab decomposition because the windows are global).
+    L->avs_win = std::max(0, env_int("DGB_AVS_WIN", 0));
+    {
+      const int W = L->avs_win;
+      const int nq = 1 << d;
+      const int nw = (W > 0 && vlo <= vhi) ? (vhi - 1) / W - (vlo - 1) / W + 1 : 1;
+      const int w0 = (W > 0 && vlo <= vhi) ? (vlo - 1) / W : 0;
+      for (int w = 0; w < nw; ++w)
+        for (int q = 0; q < nq; ++q) {
+          std::vector<int32_t> lst;
+          for (int k = 2 * q; k <= 2 * q + 1; ++k)
+            for (int32_t e : pcp[k]) {
+              const int vl = (d == 3) ? (e >> 20) & 1023 : (e >> 10) & 1023;
+              if (W <= 0 || (vl - 1) / W == w0 + w) lst.push_back(e);
+            }
+          if (lst.empty()) continue;
+          DevList dl;
+          int rc = upload_list(lst, &dl);
+          L->pwin_pk.push_back(dl);
+          if (rc) { free_level(L); return rc; }
+        }
+    }
     for (int k = 0; k < ncol; ++k) {
       if (pc[k].empty()) continue;
       DevList a, b, ap, bp;
@@ -800,7 +833,8 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
         }
         return DG_OK;
       }
-      for (auto& c : L->pcol_pk) {
+      const auto& order = env_int("DGB_AVS_COLOURS", 0) ? L->pcol_pk : L->pwin_pk;
+      for (auto& c : order) {
         ++*nl;
         if ((rc = patch_fdm_packed(L, r, x, omega, c, st))) return rc;
       }

@@ -332,6 +332,34 @@ def test_single_launch_atomic_avs_matches_colour_launches(d, nc, k, monkeypatch)
     assert rel(xb - x0, xa - x0) <= 1e-13
 
 
+@pytest.mark.parametrize("d,nc,k", [(3, 12, 3), (3, 9, 5), (2, 21, 4), (3, 7, 7)])
+def test_parity_class_launches_bitwise_equal_colour_launches(d, nc, k, monkeypatch):
+    """The additive step launches colours 2q and 2q+1 together (same vertex
+    parity: write-disjoint); every dof keeps its update order, so the result
+    is bitwise the 16-colour sequence.  z-windowed class order (DGB_AVS_WIN)
+    changes only the order of boundary-layer updates (rounding)."""
+    monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
+    monkeypatch.setenv("DGB_AVS_COLOURS", "1")
+    ctx, _, sm = _setup(d, nc, k, "avs", 0.25)
+    x0, b = inputs(ctx.ndofs, 10)
+    sm.use_graph = False
+    xa = x0.copy()
+    sm.smooth(xa, b)
+    assert ctx.dev._lib.dg_last_launch_count(ctx.dev.handle) == 1 + 2 ** (d + 1)
+    monkeypatch.setenv("DGB_AVS_COLOURS", "0")
+    xb = x0.copy()
+    sm.smooth(xb, b)
+    assert ctx.dev._lib.dg_last_launch_count(ctx.dev.handle) == 1 + 2 ** d
+    assert np.array_equal(xa, xb)
+    monkeypatch.setenv("DGB_AVS_WIN", "2")
+    ctx2, _, sm2 = _setup(d, nc, k, "avs", 0.25)
+    xc = x0.copy()
+    sm2.smooth(xc, b)
+    assert rel(xc - x0, xa - x0) <= 1e-14
+    want = OracleLevel((nc,) * d, k).smooth("avs", 0.25, x0, b)
+    assert rel(xc, want) <= RTOL
+
+
 def test_local_solver_apply_inverse_is_exact_local_solve():
     """`LocalSolver.apply_inverse` (fastdiag.py:118-133) on the device: the
     cell solver inverts the Kronecker-sum cell matrix, the patch solver the
