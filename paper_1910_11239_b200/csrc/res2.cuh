@@ -58,11 +58,27 @@ template <int D, int N, int G>
 struct RLay {
   using L = Lay<D, N>;
   static constexpr int F = L::F;
-  static constexpr int GS = L::SZ;
-  __device__ __forceinline__ static int sstride(int t) { return L::sstride(t); }
-  __device__ __forceinline__ static int sbase(int t, int f) { return L::sbase(t, f); }
+  // 3D n = 6 (cfg 5): row pitch 9 and plane pitch 54 instead of 7 / 42 make
+  // the direction-1 fibers bank-conflict free as well (shared wavefronts per
+  // cell group 504 -> 396, the residual is L1/shared-pipe bound); the
+  // direction-2 fibers stay 2-way (no straight layout frees all three)
+  static constexpr bool WIDE = (D == 3 && N == 6);
+  static constexpr int P = WIDE ? 9 : L::P;
+  static constexpr int Q = WIDE ? 54 : L::P * N;
+  static constexpr int GS = (D == 3) ? Q * N : L::SZ;
+  __device__ __forceinline__ static int sstride(int t) {
+    if (D == 2) return L::sstride(t);
+    return t == 0 ? 1 : (t == 1 ? P : Q);
+  }
+  __device__ __forceinline__ static int sbase(int t, int f) {
+    if (D == 2) return L::sbase(t, f);
+    const int a = f % N, b = f / N;
+    if (t == 0) return a * P + b * Q;
+    if (t == 1) return a + b * Q;
+    return a + b * P;
+  }
   // shared offset of cell row w (direction-0 fiber w = i1 + n i2)
-  __device__ __forceinline__ static int row(int w) { return L::sbase(0, w); }
+  __device__ __forceinline__ static int row(int w) { return sbase(0, w); }
   __device__ __forceinline__ static void who(int, int tid, int& g, int& f) {
     g = tid / F;
     f = tid - g * F;
