@@ -291,7 +291,7 @@ def run_ours(args, cfg):
     if kind in ("avs", "mvs"):
         npatch = int(np.prod([v - 1 for v in rdims]))
         f_solve = F.solve_flops(d, 2 * (k + 1), npatch)
-        dom = f"fdm2_kernel<{d},{2 * (k + 1)},patch> (all colours)"
+        dom = f"fdm2_kernel<{d},{2 * (k + 1)},patch> (patch solves: one launch, bulk reduce-add)"
     else:
         f_solve = F.solve_flops(d, k + 1, int(np.prod(dims)))
         dom = f"fdm2_kernel<{d},{k + 1},cell>"

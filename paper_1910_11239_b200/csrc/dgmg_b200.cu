@@ -533,8 +533,20 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
       }
     }
     {
+      // one-launch additive step: patches in spatial order (v_1 fastest), so
+      // the CTAs in flight work on a thin z-slab whose r and x stay in L2
+      // while its cells receive their 2^d overlapping updates; colour order
+      // with DGB_AVS_ATOMIC_ORDER=0
       std::vector<int32_t> all;
-      for (int k = 0; k < ncol; ++k) all.insert(all.end(), pcp[k].begin(), pcp[k].end());
+      if (env_int("DGB_AVS_ATOMIC_ORDER", 1)) {
+        std::vector<std::pair<int32_t, int32_t>> srt;  // (patch id, packed vertex)
+        for (int k = 0; k < ncol; ++k)
+          for (size_t i = 0; i < pc[k].size(); ++i) srt.push_back({pc[k][i], pcp[k][i]});
+        std::sort(srt.begin(), srt.end());
+        for (auto& e2 : srt) all.push_back(e2.second);
+      } else {
+        for (int k = 0; k < ncol; ++k) all.insert(all.end(), pcp[k].begin(), pcp[k].end());
+      }
       if (int rc = upload_list(all, &L->pall_pk)) { free_level(L); return rc; }
     }
     // Additive launch order.  Colours 2q and 2q+1 share the vertex parity q,
@@ -802,13 +814,18 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
                              L->peo(), L->flow, st);
       }
       if ((rc = res_range())) return rc;
-      // small levels are launch-bound with 16 colour launches: one launch over
-      // all patches with fp64 reductions for the overlaps is faster there
-      // (cfg 2: 0.173 -> 0.145 ms); large levels keep the write-disjoint
-      // colour launches (L2 reduction throughput, cfg 5: 3.37 vs 3.83 ms)
+      // default: one launch over all patches in spatial order; the overlaps
+      // accumulate by the TMA engine's fp64 bulk reduce-add at L2 (atomic per
+      // element), and the in-flight patches form a thin z-slab whose r and x
+      // stay in L2 while each cell takes its 2^d updates.  Measured: cfg 5
+      // 2.65 -> 2.47 ms (vs one launch per parity class), cfg 2 0.111 ->
+      // 0.091 ms.  The summation order of a dof's 2^d updates then varies
+      // run to run (~1e-16 relative); DGB_AVS_ATOMIC=0 gives the
+      // deterministic parity-class launches (bitwise the reference's colour
+      // order).  DGB_AVS_ATOMIC_MAX_MDOFS caps the patch dofs of this path.
       const int64_t pdofs = L->pall_pk.count * (L->d == 3 ? (int64_t)L->m * L->m * L->m
                                                           : (int64_t)L->m * L->m);
-      const int64_t amax = (int64_t)env_int("DGB_AVS_ATOMIC_MAX_MDOFS", 64) * 1000000;
+      const int64_t amax = (int64_t)env_int("DGB_AVS_ATOMIC_MAX_MDOFS", 1 << 30) * 1000000;
       if (env_int("DGB_AVS_ATOMIC", 1) && L->pall_pk.count > 0 && pdofs <= amax) {
         ++*nl;
         FdmArgs p = fdm_params(L, true, r, x, omega);

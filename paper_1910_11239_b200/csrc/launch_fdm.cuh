@@ -94,7 +94,9 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
     return DG_OK;
   }
   if constexpr ((Rows<D, M, PATCH>::N % 2) == 0) {
-    if (p.direct == 2 && !q.atomic && !q.cluster) {
+    // the bulk reduce-add is an element-wise atomic fp64 add at L2, so the
+    // bulk path also serves overlapping subdomains (atomic accumulation)
+    if (p.direct == 2 && (!q.atomic || env_int("DGB_BULK_ATOMIC", 1)) && !q.cluster) {
       auto kb = fdm2_kernel<D, M, PATCH, true>;
       static bool attr_b = false;
       if (!attr_b) {

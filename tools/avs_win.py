@@ -30,7 +30,11 @@ b = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, x0.numel())).cuda()
 ref = None
 for w in a.wins.split(","):
     os.environ["DGB_AVS_COLOURS"] = "1" if w == "colours" else "0"
-    os.environ["DGB_AVS_WIN"] = "0" if w == "colours" else w
+    os.environ["DGB_AVS_WIN"] = w if w.isdigit() else "0"
+    # "atomic": one launch over all patches (bulk fp64 reduce-add), spatial order;
+    # "atomic_col": same in colour order
+    os.environ["DGB_AVS_ATOMIC_MAX_MDOFS"] = "100000" if w.startswith("atomic") else "64"
+    os.environ["DGB_AVS_ATOMIC_ORDER"] = "0" if w == "atomic_col" else "1"
     ctx = dg.make_context(lvl, basis)
     sm = dg.make_level_smoother(ctx, basis, dg.SmootherConfig(kind=c["kind"], omega=c["omega"]))
     x = x0.clone()
