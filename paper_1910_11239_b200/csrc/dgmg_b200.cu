@@ -112,6 +112,10 @@ struct dg_level {
   std::vector<DevList> clus_pk;     // AVS clusters per cluster colour, packed base vertices
   DevList pall_pk;                  // all patches (colour order), packed, one-launch AVS
   std::vector<DevList> pwin_pk;     // AVS launch order: (z-window, parity class), packed
+  int pall_vlo = 0;                 // first v_last of pall_pk (spatial order)
+  int64_t layer_patches = 0;        // patches per v_last value
+  cudaStream_t side = nullptr;      // low-priority stream of the overlapped AVS residual
+  std::vector<cudaEvent_t> ev;      // residual-chunk completion events
   int avs_win = 0;                  // z-window of pwin_pk in patch vertices (0 = whole level)
   FlowDev flow;                     // dataflow AVS step (flow.cuh)
   bool flow_ok = false;
@@ -142,6 +146,8 @@ static void free_level(dg_level* L) {
   cudaFree(L->flow.state);
   cudaFree(L->flow.state_init);
   if (L->cap) cudaStreamDestroy(L->cap);
+  if (L->side) cudaStreamDestroy(L->side);
+  for (auto e : L->ev) cudaEventDestroy(e);
   delete L;
 }
 
@@ -512,6 +518,8 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
       int64_t layer_patches = 1;
       for (int t = 0; t < d - 1; ++t) layer_patches *= (nc[t] - 1);
       const int64_t p0 = (int64_t)(vlo - 1) * layer_patches, p1 = (int64_t)vhi * layer_patches;
+      L->pall_vlo = vlo;
+      L->layer_patches = layer_patches;
       for (int64_t id = p0; id < p1; ++id) {
         int64_t rem = id;
         int v[3] = {1, 1, 1}, parq = 0, half = 0;
@@ -638,10 +646,18 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     free_level(L);
     return rc;
   }
-  e = cudaStreamCreateWithFlags(&L->cap, cudaStreamNonBlocking);
-  if (e != cudaSuccess) {
-    free_level(L);
-    return fail(DG_ECUDA, std::string("stream create: ") + cudaGetErrorString(e));
+  {
+    // the capture stream carries the patch solves at the highest priority;
+    // the residual chunks of the overlapped AVS step run on `side` at the
+    // lowest, so free CTA slots go to the solves first
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    e = cudaStreamCreateWithPriority(&L->cap, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&L->side, cudaStreamNonBlocking, lo);
+    if (e != cudaSuccess) {
+      free_level(L);
+      return fail(DG_ECUDA, std::string("stream create: ") + cudaGetErrorString(e));
+    }
   }
   *out = L;
   return DG_OK;
@@ -813,6 +829,82 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
         return dispatch_flow(L->d, L->n, ra, fa, L->hres(), L->hpz.data(), L->hpzt.data(),
                              L->peo(), L->flow, st);
       }
+      const int64_t pdofs = L->pall_pk.count * (L->d == 3 ? (int64_t)L->m * L->m * L->m
+                                                          : (int64_t)L->m * L->m);
+      const int64_t amax = (int64_t)env_int("DGB_AVS_ATOMIC_MAX_MDOFS", 1 << 30) * 1000000;
+      if (env_int("DGB_AVS_ATOMIC", 1) && L->pall_pk.count > 0 && pdofs <= amax &&
+          L->d == 3 && env_int("DGB_AVS_OVERLAP", 0)) {
+        // residual and solves overlapped in z-chunks of C cell layers on two
+        // streams: R(k) = residual on layers [z_k, z_k+1), S(k) = patches with
+        // v_z in (z_k, z_k+1] (they read r on [z_k, z_k+1] and add into x
+        // there).  S(k) waits for R(k+1): every residual that reads x on
+        // those layers (R(k-1..k+1)) is done before S(k) writes them, and
+        // R(k+2) reads layers >= z_k+2 - 1 > z_k+1, so it runs concurrently.
+        // The solves' stream has the higher priority; the residual chunks
+        // fill the CTA slots the solves leave.  Opt-in: measured no gain on
+        // cfg 5 (2.47 ms for chunks of 8/16 layers, 2.5-2.7 ms when the
+        // residual is held at most DGB_AVS_LEAD chunks ahead) -- both kernels
+        // are bound by the SM's L1/shared pipe, so running them side by side
+        // does not add throughput.
+        const int C = std::max(2, env_int("DGB_AVS_CHUNK", 8) & ~1);
+        const int z0 = L->desc.res_begin, z1 = L->desc.res_end;
+        const int K = (z1 - z0 + C - 1) / C;
+        if (K >= 3) {
+          // events: ev[0..K) residual chunks, ev[K..2K) solve chunks, fork, join
+          if ((int)L->ev.size() < 2 * K + 2) {
+            for (int i = (int)L->ev.size(); i < 2 * K + 2; ++i) {
+              cudaEvent_t e2;
+              DG_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+              L->ev.push_back(e2);
+            }
+          }
+          cudaStream_t sd = L->side;
+          DG_CUDA(cudaEventRecord(L->ev[2 * K], st));  // fork
+          DG_CUDA(cudaStreamWaitEvent(sd, L->ev[2 * K], 0));
+          auto zc = [&](int k) { return std::min(z1, z0 + k * C); };
+          auto pidx = [&](int v) {  // first index in pall_pk with v_last >= v
+            const int vv = std::max(L->pall_vlo, v);
+            return std::min<int64_t>(L->pall_pk.count, (int64_t)(vv - L->pall_vlo) * L->layer_patches);
+          };
+          // R(k) may run ahead of the solves by `lead` chunks: R(k) waits for
+          // S(k - lead - 1), so the hardware queue holds a mix of both
+          const int lead = std::max(1, env_int("DGB_AVS_LEAD", 2));
+          auto launch_r = [&](int k) -> int {
+            if (k >= K) return DG_OK;
+            if (k - lead - 1 >= 0) DG_CUDA(cudaStreamWaitEvent(sd, L->ev[K + k - lead - 1], 0));
+            ResArgs p = res_params(L, x, b, r);
+            p.start = (int64_t)(zc(k) - L->desc.z_begin) * L->layer_cells;
+            p.count = (int64_t)(zc(k + 1) - zc(k)) * L->layer_cells;
+            ++*nl;
+            if (int rc2 = dispatch_residual(L->d, L->n, p, L->hres(), sd)) return rc2;
+            DG_CUDA(cudaEventRecord(L->ev[k], sd));
+            return DG_OK;
+          };
+          for (int k = 0; k <= lead; ++k)
+            if ((rc = launch_r(k))) return rc;
+          for (int k = 0; k < K; ++k) {
+            const int64_t i0 = k == 0 ? 0 : pidx(zc(k) + 1);
+            const int64_t i1 = k == K - 1 ? L->pall_pk.count : pidx(zc(k + 1) + 1);
+            DG_CUDA(cudaStreamWaitEvent(st, L->ev[std::min(k + 1, K - 1)], 0));
+            if (i1 > i0) {
+              ++*nl;
+              FdmArgs p = fdm_params(L, true, r, x, omega);
+              p.list = L->pall_pk.ptr + i0;
+              p.count = i1 - i0;
+              p.packed = 1;
+              p.atomic = 1;
+              if ((rc = dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), L->peo(),
+                                           st)))
+                return rc;
+            }
+            DG_CUDA(cudaEventRecord(L->ev[K + k], st));
+            if ((rc = launch_r(k + lead + 1))) return rc;
+          }
+          DG_CUDA(cudaEventRecord(L->ev[2 * K + 1], sd));  // join
+          DG_CUDA(cudaStreamWaitEvent(st, L->ev[2 * K + 1], 0));
+          return DG_OK;
+        }
+      }
       if ((rc = res_range())) return rc;
       // default: one launch over all patches in spatial order; the overlaps
       // accumulate by the TMA engine's fp64 bulk reduce-add at L2 (atomic per
@@ -823,9 +915,6 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
       // run to run (~1e-16 relative); DGB_AVS_ATOMIC=0 gives the
       // deterministic parity-class launches (bitwise the reference's colour
       // order).  DGB_AVS_ATOMIC_MAX_MDOFS caps the patch dofs of this path.
-      const int64_t pdofs = L->pall_pk.count * (L->d == 3 ? (int64_t)L->m * L->m * L->m
-                                                          : (int64_t)L->m * L->m);
-      const int64_t amax = (int64_t)env_int("DGB_AVS_ATOMIC_MAX_MDOFS", 1 << 30) * 1000000;
       if (env_int("DGB_AVS_ATOMIC", 1) && L->pall_pk.count > 0 && pdofs <= amax) {
         ++*nl;
         FdmArgs p = fdm_params(L, true, r, x, omega);

@@ -360,6 +360,29 @@ def test_parity_class_launches_bitwise_equal_colour_launches(d, nc, k, monkeypat
     assert rel(xc, want) <= RTOL
 
 
+@pytest.mark.parametrize("d,nc,k,chunk", [(3, 12, 3, 2), (3, 10, 5, 4), (3, 9, 7, 2)])
+def test_overlapped_avs_step_matches_colour_launches(d, nc, k, chunk, monkeypatch):
+    """Opt-in overlapped AVS step (DGB_AVS_OVERLAP=1): residual z-chunks on a
+    second stream next to the patch-solve chunks, event dependencies keep
+    every residual ahead of the updates it reads (rounding-level equal)."""
+    monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
+    ctx, _, sm = _setup(d, nc, k, "avs", 0.25)
+    x0, b = inputs(ctx.ndofs, 12)
+    xa = x0.copy()
+    sm.smooth(xa, b)
+    monkeypatch.setenv("DGB_AVS_ATOMIC", "1")
+    monkeypatch.setenv("DGB_AVS_OVERLAP", "1")
+    monkeypatch.setenv("DGB_AVS_CHUNK", str(chunk))
+    for lead in ("1", "2"):
+        monkeypatch.setenv("DGB_AVS_LEAD", lead)
+        ctx2, _, sm2 = _setup(d, nc, k, "avs", 0.25)
+        sm2.use_graph = lead == "1"
+        xb = x0.copy()
+        sm2.smooth(xb, b)
+        assert ctx2.dev._lib.dg_last_launch_count(ctx2.dev.handle) > 2
+        assert rel(xb - x0, xa - x0) <= 1e-14
+
+
 def test_local_solver_apply_inverse_is_exact_local_solve():
     """`LocalSolver.apply_inverse` (fastdiag.py:118-133) on the device: the
     cell solver inverts the Kronecker-sum cell matrix, the patch solver the

@@ -35,6 +35,11 @@ for w in a.wins.split(","):
     # "atomic_col": same in colour order
     os.environ["DGB_AVS_ATOMIC_MAX_MDOFS"] = "100000" if w.startswith("atomic") else "64"
     os.environ["DGB_AVS_ATOMIC_ORDER"] = "0" if w == "atomic_col" else "1"
+    # "ovN": overlapped residual/solve chunks of N layers; "atomic": no overlap
+    os.environ["DGB_AVS_OVERLAP"] = "1" if w.startswith("ov") else "0"
+    if w.startswith("ov"):
+        os.environ["DGB_AVS_CHUNK"] = w[2:]
+        os.environ["DGB_AVS_ATOMIC_MAX_MDOFS"] = "100000"
     ctx = dg.make_context(lvl, basis)
     sm = dg.make_level_smoother(ctx, basis, dg.SmootherConfig(kind=c["kind"], omega=c["omega"]))
     x = x0.clone()
