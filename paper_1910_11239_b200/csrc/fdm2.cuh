@@ -700,11 +700,15 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
   }
 }
 
-// bulk variant: register budget of 56 per thread (4 CTAs of 288 threads per SM)
+// bulk variant: register budget of 56 per thread (4 CTAs of 288 threads per SM;
+// 5 CTAs would mean 40 registers and ~1 KB of spills per thread at m = 12)
+#ifndef FDM_BULK_REGS
+#define FDM_BULK_REGS 56
+#endif
 template <int D, int M>
 __host__ __device__ constexpr int fdm2_min_ctas(bool bulk) {
-  return bulk ? (65536 / (fdm2_groups<D, M>() * Lay<D, M>::F * 56) > 0
-                     ? 65536 / (fdm2_groups<D, M>() * Lay<D, M>::F * 56)
+  return bulk ? (65536 / (fdm2_groups<D, M>() * Lay<D, M>::F * FDM_BULK_REGS) > 0
+                     ? 65536 / (fdm2_groups<D, M>() * Lay<D, M>::F * FDM_BULK_REGS)
                      : 1)
               : 0;  // 0: no minimum (ptxas default heuristics)
 }
