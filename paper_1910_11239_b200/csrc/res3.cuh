@@ -219,8 +219,9 @@ res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
     mass3<N>(p, v, o);        // c = M_1 a + G_1 b
 #pragma unroll
     for (int k = 0; k < N; ++k) A[sb + k * ss] = o[k] + t[k];
-    // right-hand side along the t = 2 fiber (i0, i1) = (fa, fb)
-    if (p.b) {
+    // right-hand side along the t = 2 fiber (i0, i1) = (fa, fb), prefetched
+    // across the barrier (n <= 6: loaded in the last pass, fewer registers)
+    if (N > 6 && p.b) {
 #pragma unroll
       for (int k = 0; k < N; ++k) bq[k] = __ldg(p.b + cb + fa + N * fb + N * N * k);
     }
@@ -241,6 +242,10 @@ res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
     for (int k = 0; k < N; ++k) v[k] = A[sb + k * ss];
     mass3<N>(p, v, o);        // M_2 c
     double* r = p.r + cb + fa + N * fb;
+    if (N <= 6 && p.b) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) bq[k] = __ldg(p.b + cb + fa + N * fb + N * N * k);
+    }
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       const double ax = o[k] + t[k];

@@ -56,7 +56,7 @@ def test_operator_matches_oracle_at_size(d, nc, k):
     assert rel(dg.residual(ctx, x0, b, out=r), lvl.residual(x0, b)) <= RTOL
 
 
-@pytest.mark.parametrize("k", [3, 5, 6, 7])
+@pytest.mark.parametrize("k", [3, 5, 6, 7, 8, 11, 12, 15])
 def test_residual_kernel_variants_agree(k, monkeypatch):
     """res2 (five passes) and res3 (three passes, mass-transformed face
     fields) regroup the same sums: equal to rounding, and both at the oracle."""
@@ -66,6 +66,7 @@ def test_residual_kernel_variants_agree(k, monkeypatch):
     got = {}
     for v in ("0", "1"):
         monkeypatch.setenv("DGB_RES3", v)
+        monkeypatch.setenv("DGB_RES3_HI", v)
         got[v] = dg.residual(ctx, x0, b, out=np.empty(ctx.ndofs))
         assert rel(got[v], want) <= RTOL
     assert rel(got["0"], got["1"]) <= 1e-14
