@@ -124,6 +124,16 @@ int dg_patch_fdm(const dg_level_t* lvl, const double* r, double* x,
                  double omega, const int32_t* patches, int64_t n_patches,
                  int atomic, void* stream);
 
+/* Additive local solves restricted to a range of layers along the last
+ * direction, for pipelined steps (host copies overlapped with compute):
+ * DG_ACS: x += omega A_c^{-1} r_c for the owned cells with c_last in [lo, hi);
+ * DG_AVS: x += omega R_j^T A_j^{-1} R_j r for the patches with last vertex
+ * coordinate in [lo, hi), accumulated by fp64 bulk reduce-add (overlapping
+ * patches may run concurrently).  (CellSolverSet / PatchSolverSet
+ * .solve_partitioned, fastdiag.py:457-496, 602-628)                       */
+int dg_solve_range(const dg_level_t* lvl, int kind, double omega, const double* r,
+                   double* x, int lo, int hi, void* stream);
+
 /* colour lists built at create time (device int32, owned by the level)     */
 int dg_num_colours(const dg_level_t* lvl, int kind);
 int dg_colour_list(const dg_level_t* lvl, int kind, int colour,

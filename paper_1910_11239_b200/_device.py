@@ -1,8 +1,10 @@
 """Device plumbing: torch for memory and streams, nothing else.
 
-The public API accepts numpy arrays (copied host<->device around the call, so
-that callers written for the reference, e.g. its V-cycle, work unchanged) and
-torch float64 CUDA tensors (zero-copy, ordered on the current stream).
+The public API accepts numpy arrays and CPU (e.g. pinned) torch tensors
+(copied host<->device around the call, so that callers written for the
+reference, e.g. its V-cycle, work unchanged; additive steps pipeline those
+copies against the kernels, smoothers.LevelSmoother._host_step) and torch
+float64 CUDA tensors (zero-copy, ordered on the current stream).
 """
 
 from __future__ import annotations
@@ -31,9 +33,18 @@ class Staged:
 
     def __init__(self, a, ndofs: int, name: str, need_copy: bool = True,
                  staging: torch.Tensor | None = None):
+        if isinstance(a, torch.Tensor) and not a.is_cuda:
+            # host tensor (e.g. pinned): staged like a numpy array, written back
+            if a.dtype != torch.float64 or a.numel() != ndofs:
+                raise ValueError(f"{name}: expected a float64 vector of the level size")
+            self.host = a
+            if staging is None:
+                staging = torch.empty(ndofs, dtype=torch.float64, device="cuda")
+            if need_copy:
+                staging.copy_(a.reshape(-1), non_blocking=False)
+            self.dev = staging
+            return
         if isinstance(a, torch.Tensor):
-            if not a.is_cuda:
-                raise ValueError(f"{name}: torch tensors must live on a CUDA device")
             if a.dtype != torch.float64:
                 raise ValueError(f"{name}: expected float64")
             if a.numel() != ndofs:
@@ -59,6 +70,9 @@ class Staged:
         return self.dev.data_ptr()
 
     def finish(self) -> None:
+        if isinstance(self.host, torch.Tensor):
+            self.host.view(-1).copy_(self.dev)
+            return
         if self.host is not None:
             out = self.dev.cpu().numpy()
             if self.host.flags.writeable:

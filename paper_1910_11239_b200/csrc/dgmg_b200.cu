@@ -734,6 +734,44 @@ int dg_patch_fdm(const dg_level_t* L, const double* r, double* x, double omega,
   return dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), L->peo(), (cudaStream_t)stream);
 }
 
+int dg_solve_range(const dg_level_t* L, int kind, double omega, const double* r, double* x,
+                   int lo, int hi, void* stream) {
+  if (!L || !r || !x) return fail(DG_EINVAL, "null argument");
+  if (r == x) return fail(DG_EINVAL, "solve: r must not alias x");
+  if (int rc = check_align(L, r, x, nullptr)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kind == DG_ACS) {
+    // cells of owned layers [lo, hi)
+    const int z0 = std::max(lo, L->desc.own_begin), z1 = std::min(hi, L->desc.own_end);
+    if (z1 <= z0) return DG_OK;
+    FdmArgs p = fdm_params(L, false, r, x, omega);
+    p.start = (int64_t)(z0 - L->desc.z_begin) * L->layer_cells;
+    p.count = (int64_t)(z1 - z0) * L->layer_cells;
+    return dispatch_cell_fdm(L->d, L->n, p, L->hcz.data(), L->hczt.data(), L->ceo(), st);
+  }
+  if (kind == DG_AVS) {
+    // patches with last vertex coordinate in [lo, hi): a contiguous range of
+    // the spatially ordered all-patch list, overlaps by bulk reduce-add
+    if (!L->has_patch) return fail(DG_EUNSUPPORTED, "vertex patches unsupported here");
+    if (!env_int("DGB_AVS_ATOMIC_ORDER", 1))
+      return fail(DG_EINVAL, "dg_solve_range needs the spatial patch order");
+    if (L->pall_pk.count == 0) return DG_OK;
+    auto idx = [&](int v) {
+      const int vv = std::max(L->pall_vlo, v);
+      return std::min<int64_t>(L->pall_pk.count, (int64_t)(vv - L->pall_vlo) * L->layer_patches);
+    };
+    const int64_t i0 = idx(lo), i1 = idx(hi);
+    if (i1 <= i0) return DG_OK;
+    FdmArgs p = fdm_params(L, true, r, x, omega);
+    p.list = L->pall_pk.ptr + i0;
+    p.count = i1 - i0;
+    p.packed = 1;
+    p.atomic = 1;
+    return dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), L->peo(), st);
+  }
+  return fail(DG_EINVAL, "dg_solve_range: kind must be DG_ACS or DG_AVS");
+}
+
 int dg_num_colours(const dg_level_t* L, int kind) {
   if (!L) return -1;
   switch (kind) {

@@ -323,6 +323,7 @@ def test_single_launch_atomic_avs_matches_colour_launches(d, nc, k, monkeypatch)
     ctx, _, sm = _setup(d, nc, k, "avs", 0.25)
     sm.use_graph = False
     x0, b = inputs(ctx.ndofs, 9)
+    monkeypatch.setenv("DGB_HOST_PIPELINE", "0")  # numpy inputs: the one-launch device step
     monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
     xa = x0.copy()
     sm.smooth(xa, b)
@@ -367,6 +368,7 @@ def test_overlapped_avs_step_matches_colour_launches(d, nc, k, chunk, monkeypatc
     second stream next to the patch-solve chunks, event dependencies keep
     every residual ahead of the updates it reads (rounding-level equal)."""
     monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
+    monkeypatch.setenv("DGB_HOST_PIPELINE", "0")  # numpy inputs: the device step
     ctx, _, sm = _setup(d, nc, k, "avs", 0.25)
     x0, b = inputs(ctx.ndofs, 12)
     xa = x0.copy()
@@ -382,6 +384,30 @@ def test_overlapped_avs_step_matches_colour_launches(d, nc, k, chunk, monkeypatc
         sm2.smooth(xb, b)
         assert ctx2.dev._lib.dg_last_launch_count(ctx2.dev.handle) > 2
         assert rel(xb - x0, xa - x0) <= 1e-14
+
+
+@pytest.mark.parametrize("kind,omega,k", [("avs", 0.25, 3), ("acs", 0.7, 3), ("avs", 0.25, 5)])
+def test_host_pipelined_step_matches_device_step(kind, omega, k):
+    """Host vectors (numpy, pinned tensors) take the pipelined path: chunked
+    H2D / residual / range solves / D2H; equal to the device-resident step
+    (ACS bitwise, AVS to rounding: one-launch AVS accumulates atomically)."""
+    nc = 24
+    ctx, _, sm = _setup(3, nc, k, kind, omega)
+    x0, b = inputs(ctx.ndofs, 13)
+    assert sm._pipelinable(x0, b)
+    xd = torch.from_numpy(x0).cuda()
+    sm.smooth(xd, torch.from_numpy(b).cuda())
+    want = xd.cpu().numpy()
+    xn = x0.copy()
+    sm.smooth(xn, b)
+    xt = torch.from_numpy(x0.copy()).pin_memory()
+    sm.smooth(xt, torch.from_numpy(b).pin_memory())
+    for got in (xn, xt.numpy()):
+        if kind == "acs":
+            assert np.array_equal(got, want)
+        else:
+            assert rel(got - x0, want - x0) <= 1e-14
+    assert rel(xn, OracleLevel((nc,) * 3, k).smooth(kind, omega, x0, b)) <= RTOL
 
 
 def test_local_solver_apply_inverse_is_exact_local_solve():
