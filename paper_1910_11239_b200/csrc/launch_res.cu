@@ -34,7 +34,7 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
   std::memcpy(p.mats.bg1, h.bg + N, sizeof(p.mats.bg1));
   p.eo = h.eo != nullptr && N % 2 == 0;
   if (p.eo) std::memcpy(p.mats.eo, h.eo, sizeof(p.mats.eo));
-  if constexpr (D == 3 && N >= 6) {
+  if constexpr (D == 3) {
     // three-pass residual (res3.cuh) where measured faster than res2
     // (tools/res_sweep.py, ~16.8M dofs, ms res2 / res3): n = 7, 8, 9
     // (0.31 / 0.28 at n = 9) and n = 13..16 (0.32 / 0.24 at n = 16, cfg 4);
@@ -43,7 +43,7 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
     // forces res2 / res3 for n >= 9.
     constexpr bool PREF = N <= 9 || N >= 13;
     const int hi = env_int("DGB_RES3_HI", -1);
-    const bool use = N == 6 ? env_int("DGB_RES3_6", 0) != 0
+    const bool use = N <= 6 ? env_int("DGB_RES3_LO", 0) != 0
                             : (N <= 8 || (hi < 0 ? PREF : hi != 0));
     if (env_int("DGB_RES3", 1) && use) {
       using S = Res3Shape<N>;

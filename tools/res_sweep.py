@@ -33,6 +33,7 @@ for k in [int(v) for v in a.ks.split(",")]:
     ref = None
     for v in ("0", "1"):
         os.environ["DGB_RES3_HI"] = v
+        os.environ["DGB_RES3_LO"] = v
         for _ in range(3):
             dg.residual(ctx, x, b, out=r)
         torch.cuda.synchronize()
