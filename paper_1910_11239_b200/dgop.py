@@ -37,6 +37,7 @@ __all__ = [
     "apply_operator",
     "residual",
     "assemble_dense",
+    "compute_rhs",
 ]
 
 
@@ -264,3 +265,90 @@ def assemble_dense(ctx: OperatorContext, via: str = "kronecker", device=None):
     perm = torch.from_numpy(jdm).to(dev)
     a = a.index_select(0, perm).index_select(1, perm)
     return a.numpy() if device is None else a
+
+
+def _contract_quad(w: torch.Tensor, vals: torch.Tensor, k: int) -> torch.Tensor:
+    """(B, q_1..q_k) reversed quadrature layout -> (B, n_k..n_1) canonical:
+    out[b, i_k..i_1] = sum_q prod_t phi_{i_t}(x_{q_t}) w[b, q_1..q_k]
+    (`_tensor.backward_all`, `_tensor.py:81-97`)."""
+    y = w
+    for _ in range(k):
+        # contract the current first quadrature axis (after the batch), append
+        # the node axis at the end, so the node axes come out n_1 .. n_k
+        y = torch.tensordot(y, vals, dims=([1], [1]))
+    # y: (B, n_1, .., n_k) -> canonical (B, n_k, .., n_1)
+    return y.permute(0, *range(k, 0, -1)).contiguous() if k > 1 else y
+
+
+def compute_rhs(ctx: OperatorContext, f, g):
+    """Load vector (`dgop.py:800-871`): volume source f plus the Nitsche
+    boundary terms of the Dirichlet data g with the operator's penalty and
+    trace weights, on a Cartesian level.  f and g are the reference's host
+    callables on (N, d) coordinate arrays; their values at the quadrature
+    points are contracted with the basis on the device (sum factorisation).
+    Returns a numpy vector in the canonical layout."""
+    require_cuda()
+    lay = ctx.layout
+    d, n, dims = lay.dim, lay.n1d, lay.dims
+    b = ctx.basis
+    h = float(ctx.tables.h)
+    qp, qw = np.asarray(b.qpts, float), np.asarray(b.qwts, float)
+    nq = qp.size
+    dev = torch.device("cuda")
+    vals = torch.from_numpy(np.ascontiguousarray(b.values)).to(dev)      # (n, nq)
+    # cell origins, cell id order (direction 1 fastest)
+    cidx = np.indices(tuple(dims[::-1])).reshape(d, -1)[::-1].T            # (ncells, d)
+    origin = cidx * h
+    # volume: reversed quadrature layout (q_1 slowest), column t = direction t+1
+    ref = np.stack([g_.ravel() for g_ in np.meshgrid(*([qp] * d), indexing="ij")], axis=-1)
+    wq = np.ones(1)
+    for _ in range(d):
+        wq = np.multiply.outer(wq, qw).ravel()
+    coords = origin[:, None, :] + h * ref[None, :, :]
+    fv = np.asarray(f(coords.reshape(-1, d)), dtype=float).reshape(lay.ncells, -1)
+    w = torch.from_numpy(fv * (h ** d * wq)[None, :]).to(dev)
+    rhs = _contract_quad(w.reshape((lay.ncells,) + (nq,) * d), vals, d)
+    rhs = rhs.reshape(lay.ncells, -1)
+    # boundary faces: Nitsche terms gamma_e |N| w g v + (-s) |N|/h w g dv/dn
+    gamma_e = sipg_penalty(ctx.gamma_hat, lay.degree, h, h)
+    area = h ** (d - 1)
+    t_full = area / h
+    bv = torch.from_numpy(np.asarray(b.bv, float)).to(dev)
+    bg = torch.from_numpy(np.asarray(b.bg, float)).to(dev)
+    for tau in range(1, d + 1):
+        trans = [t for t in range(1, d + 1) if t != tau]
+        if trans:
+            tref = np.stack([g_.ravel() for g_ in np.meshgrid(*([qp] * len(trans)),
+                                                               indexing="ij")], axis=-1)
+            wf = np.ones(1)
+            for _ in trans:
+                wf = np.multiply.outer(wf, qw).ravel()
+        else:
+            tref, wf = np.zeros((1, 0)), np.ones(1)
+        for p in (0, 1):
+            sel = cidx[:, tau - 1] == (0 if p == 0 else dims[tau - 1] - 1)
+            ids = np.nonzero(sel)[0]
+            fref = np.empty((tref.shape[0], d))
+            for j, t in enumerate(trans):
+                fref[:, t - 1] = tref[:, j]
+            fref[:, tau - 1] = float(p)
+            fc = origin[ids][:, None, :] + h * fref[None, :, :]
+            gv = np.asarray(g(fc.reshape(-1, d)), dtype=float).reshape(len(ids), -1)
+            sign = 1.0 if p == 1 else -1.0
+            mv = torch.from_numpy(gv * (gamma_e * area * wf)[None, :]).to(dev)
+            mg = torch.from_numpy(gv * (-sign * t_full * wf)[None, :]).to(dev)
+            k = len(trans)
+            if k:
+                tv = _contract_quad(mv.reshape((len(ids),) + (nq,) * k), vals, k)
+                tg = _contract_quad(mg.reshape((len(ids),) + (nq,) * k), vals, k)
+            else:
+                tv, tg = mv, mg
+            # contrib[c, nodes] with the normal node axis of tau inserted
+            tv = tv.reshape((len(ids),) + (n,) * k)
+            tg = tg.reshape((len(ids),) + (n,) * k)
+            ax = 1 + (d - tau)  # canonical node axis of direction tau
+            contrib = (tv.unsqueeze(ax) * bv[p].reshape([1] * ax + [n] + [1] * (d - ax))
+                       + tg.unsqueeze(ax) * bg[p].reshape([1] * ax + [n] + [1] * (d - ax)))
+            flat = rhs.view(lay.ncells, -1)
+            flat[torch.from_numpy(ids).to(dev)] += contrib.reshape(len(ids), -1)
+    return rhs.reshape(-1).cpu().numpy()

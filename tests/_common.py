@@ -51,3 +51,13 @@ def golden_mg():
 def useed(n, seed):
     """default_rng(seed).uniform(-1, 1, n) (tests/golden/make_golden_mg.py)."""
     return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+def rhs_f(x):
+    """Source term of the compute_rhs fixtures (tests/golden/make_golden_mg.py)."""
+    return np.sin(np.pi * x[:, 0]) * np.cos(0.5 * np.pi * x[:, -1]) + 0.25 * x.sum(axis=1)
+
+
+def rhs_g(x):
+    """Dirichlet data of the compute_rhs fixtures."""
+    return x[:, 0] ** 2 - 0.5 * x[:, -1] + 0.125

@@ -14,7 +14,9 @@ by the tests, not stored):
 - direct coarse solves (`multigrid.py:148-293`), and the Chebyshev-CG one;
 - V-cycle applications (`multigrid.py:326-350`) for all four smoother kinds;
 - V-cycle-preconditioned CG residual histories and fractional iteration
-  counts (`krylov.py:69-123`), the quantity of acceptance criteria 3-5.
+  counts (`krylov.py:69-123`), the quantity of acceptance criteria 3-5;
+- load vectors `compute_rhs(ctx, f, g)` (`dgop.py:800-871`) for the source
+  and Dirichlet data RHS_F / RHS_G below (tests/_common.py repeats them).
 """
 
 from __future__ import annotations
@@ -43,6 +45,19 @@ PCGS = [("cg_acs_2d_q3_L3", 2, 2, 3, 3, "acs", 0.7),
         ("cg_mcs_2d_q3_L3", 2, 2, 3, 3, "mcs", 1.0),
         ("cg_mvs_2d_q3_L3", 2, 2, 3, 3, "mvs", 1.0),
         ("cg_mvs_3d_q3_L1", 3, 2, 1, 3, "mvs", 1.0)]
+
+
+def RHS_F(x):
+    return np.sin(np.pi * x[:, 0]) * np.cos(0.5 * np.pi * x[:, -1]) + 0.25 * x.sum(axis=1)
+
+
+def RHS_G(x):
+    return x[:, 0] ** 2 - 0.5 * x[:, -1] + 0.125
+
+
+# (name, dim, ncells_dim, k)
+RHS = [("rhs_2d_q3_n4", 2, 4, 3), ("rhs_3d_q2_n3", 3, 3, 2), ("rhs_3d_q5_n2", 3, 2, 5),
+       ("rhs_1d_q4_n5", 1, 5, 4)]
 
 
 def main() -> None:
@@ -102,6 +117,9 @@ def main() -> None:
         out[name + "/x"] = res.x
         out[name + "/nu_frac"] = np.array([res.nu_frac, res.iterations])
         out[name + "/meta"] = np.array([d, nc, lv, k, om])
+    for name, d, nc, k in RHS:
+        ctx = dgop.make_context(mesh.build_hierarchy(d, nc, 0).levels[0], Basis1D.make(k), 1.0)
+        out[name + "/rhs"] = dgop.compute_rhs(ctx, RHS_F, RHS_G)
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT}: {len(out)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")
 

@@ -292,3 +292,17 @@ def test_fused_cg_kernels_match_torch():
         assert torch.allclose(p, z - 0.5 * p0, rtol=1e-15, atol=1e-15)
         # deterministic reductions
         assert f.dot(p, ap) == f.dot(p, ap)
+
+
+@pytest.mark.parametrize("name", sorted({k.split("/")[0] for k in G if k.startswith("rhs_")}))
+def test_compute_rhs_matches_reference(name):
+    """`dgop.compute_rhs` (`dgop.py:800-871`): volume source and Nitsche
+    boundary data contracted on the device, against the reference's vector."""
+    from _common import rhs_f, rhs_g
+    _, d, k, nc = name.split("_")
+    d, k, nc = int(d[0]), int(k[1:]), int(nc[1:])
+    basis = dg.Basis1D.make(k)
+    ctx = dg.make_context(dg.build_hierarchy(d, nc, 0).levels[0], basis, 1.0)
+    got = dgop.compute_rhs(ctx, rhs_f, rhs_g)
+    assert got.shape == (ctx.ndofs,)
+    assert rel(got, G[name + "/rhs"]) <= 1e-13
