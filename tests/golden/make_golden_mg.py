@@ -16,7 +16,9 @@ by the tests, not stored):
 - V-cycle-preconditioned CG residual histories and fractional iteration
   counts (`krylov.py:69-123`), the quantity of acceptance criteria 3-5;
 - load vectors `compute_rhs(ctx, f, g)` (`dgop.py:800-871`) for the source
-  and Dirichlet data RHS_F / RHS_G below (tests/_common.py repeats them).
+  and Dirichlet data RHS_F / RHS_G below (tests/_common.py repeats them);
+- `bench.run_experiment` records (iterations, fractional iteration count,
+  residual reduction) of the manufactured-problem solves at small levels.
 """
 
 from __future__ import annotations
@@ -58,6 +60,12 @@ def RHS_G(x):
 # (name, dim, ncells_dim, k)
 RHS = [("rhs_2d_q3_n4", 2, 4, 3), ("rhs_3d_q2_n3", 3, 3, 2), ("rhs_3d_q5_n2", 3, 2, 5),
        ("rhs_1d_q4_n5", 1, 5, 4)]
+
+
+# (name, dim, k, level_min, level_max, smoother)
+EXPERIMENTS = [("ex_acs_2d_k3", 2, 3, 3, 4, "acs"), ("ex_mcs_2d_k3", 2, 3, 3, 4, "mcs"),
+               ("ex_mvs_2d_k3", 2, 3, 3, 4, "mvs"), ("ex_avs_2d_k3", 2, 3, 3, 3, "avs"),
+               ("ex_mvs_3d_k2", 3, 2, 1, 2, "mvs"), ("ex_acs_3d_k3", 3, 3, 1, 1, "acs")]
 
 
 def main() -> None:
@@ -120,6 +128,12 @@ def main() -> None:
     for name, d, nc, k in RHS:
         ctx = dgop.make_context(mesh.build_hierarchy(d, nc, 0).levels[0], Basis1D.make(k), 1.0)
         out[name + "/rhs"] = dgop.compute_rhs(ctx, RHS_F, RHS_G)
+    from dgmg.bench import ExperimentConfig, run_experiment
+    for name, d, k, l0, l1, smoother in EXPERIMENTS:
+        recs = run_experiment(ExperimentConfig(dim=d, degree=k, level_min=l0, level_max=l1,
+                                               smoother=smoother))
+        out[name + "/records"] = np.array([[r.level, r.iterations, r.nu_frac, float(r.converged)]
+                                           for r in recs])
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT}: {len(out)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")
 

@@ -1,0 +1,31 @@
+"""Reproduce the reference's Cartesian iteration-count runs (acceptance
+criteria 3-5, `test_acceptance.py:111-181`) on the device and print one JSON
+line per level: smoother, dims, dofs, iterations, fractional count, wall time.
+
+    python tools/acceptance.py
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_1910_11239_b200.experiment import ExperimentConfig, run_experiment  # noqa: E402
+
+TARGETS = {"acs_2d_k3": 14.5, "mcs_2d_k3": 7.3, "mvs_2d_k3": 2.5, "acs_2d_k7": 18.7,
+           "mcs_2d_k7": 9.7, "mvs_2d_k7": 2.1, "acs_3d_k3": 17.1, "mcs_3d_k3": 8.6,
+           "mvs_3d_k3": 2.4}
+RUNS = (("acs_2d_k3", 2, 3, 6, 8), ("mcs_2d_k3", 2, 3, 6, 8), ("mvs_2d_k3", 2, 3, 6, 8),
+        ("acs_2d_k7", 2, 7, 7, 7), ("mcs_2d_k7", 2, 7, 7, 7), ("mvs_2d_k7", 2, 7, 7, 7),
+        ("acs_3d_k3", 3, 3, 3, 3), ("mcs_3d_k3", 3, 3, 3, 3), ("mvs_3d_k3", 3, 3, 3, 3),
+        ("avs_3d_k3", 3, 3, 3, 4), ("mvs_3d_k5", 3, 5, 3, 4))
+for key, d, k, l0, l1 in RUNS:
+    sm = key.split("_")[0]
+    for r in run_experiment(ExperimentConfig(dim=d, degree=k, level_min=l0, level_max=l1,
+                                             smoother=sm)):
+        print(json.dumps({"run": key, "level": r.level, "cells_per_dim": 2 * 2 ** r.level,
+                          "dofs": r.dofs, "solver": r.config["solver"],
+                          "iterations": r.iterations, "nu_frac": round(r.nu_frac, 3),
+                          "reference_target": TARGETS.get(key), "converged": r.converged,
+                          "wall_s": round(r.wall_time, 3)}), flush=True)
