@@ -210,6 +210,8 @@ def run_ours(args, cfg):
     torch.cuda.set_device(local)
     slab = ws > 1 or args.slab
     if slab:
+        # keep stdout to the one JSON line (NCCL prints its version otherwise)
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
         if not dist.is_initialized():
             if ws == 1:
                 os.environ.setdefault("MASTER_ADDR", "127.0.0.1")

@@ -211,6 +211,9 @@ class SlabSmoother:
         return int(self._dev._lib.dg_last_launch_count(self._dev.handle))
 
     def kernel_times(self, reps: int = 5) -> dict:
+        """Device time of the halo exchange, of the residual launch alone and
+        of the local step as `dg_smooth` issues it (direct launches); solve =
+        step - residual."""
         from . import _lib
         from ._device import stream_handle
 
@@ -218,8 +221,7 @@ class SlabSmoother:
         lib = dev._lib
         st = stream_handle()
         lay = self.layout
-        t_res = t_sol = t_x = 0.0
-        ncol = dev.num_colours("avs") if self.kind == "avs" else 1
+        t_res = t_step = t_x = 0.0
         for rep in range(reps + 1):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             ev[0].record()
@@ -228,22 +230,19 @@ class SlabSmoother:
             _lib.check(lib.dg_residual(dev.handle, self.x.data_ptr(), self.b.data_ptr(),
                                        self.r.data_ptr(), lay.res[0], lay.res[1], st))
             ev[2].record()
-            if self.kind == "avs":
-                for c in range(ncol):
-                    p, cnt = dev.colour_list("avs", c)
-                    _lib.check(lib.dg_patch_fdm(dev.handle, self.r.data_ptr(), self.x.data_ptr(),
-                                                self.omega, p, cnt, 0, st))
-            else:
-                _lib.check(lib.dg_cell_fdm(dev.handle, self.r.data_ptr(), self.x.data_ptr(),
-                                           self.omega, None, 0, st))
+            _lib.check(lib.dg_smooth(dev.handle, _lib.KINDS[self.kind], self.omega, 0,
+                                     self.x.data_ptr(), self.b.data_ptr(), self.r.data_ptr(),
+                                     0, st))
             ev[3].record()
             torch.cuda.synchronize()
             if rep:
                 t_x += ev[0].elapsed_time(ev[1])
                 t_res += ev[1].elapsed_time(ev[2])
-                t_sol += ev[2].elapsed_time(ev[3])
-        return {"halo_ms": t_x / reps, "residual_ms": t_res / reps, "solve_ms": t_sol / reps,
-                "residual_launches": 1, "solve_launches": ncol}
+                t_step += ev[2].elapsed_time(ev[3])
+        nl = int(lib.dg_last_launch_count(dev.handle))
+        return {"halo_ms": t_x / reps, "residual_ms": t_res / reps,
+                "solve_ms": (t_step - t_res) / reps, "step_direct_ms": t_step / reps,
+                "residual_launches": 1, "solve_launches": nl - 1}
 
     def e2e(self, x_owned, b_owned, reps: int = 5) -> dict:
         """Public-API step with pinned host I/O of this rank's owned x, b."""
