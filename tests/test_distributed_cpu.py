@@ -18,7 +18,7 @@ import torch.multiprocessing as mp
 
 from _common import inputs, rel
 
-from paper_1910_11239_b200.distributed import SlabLayout, SlabSmoother, halo_exchange
+from paper_1910_11239_b200.distributed import SlabLayout, SlabSmoother
 from oracle.sipg_oracle import OracleLevel
 
 

@@ -11,7 +11,6 @@ GMRES, all on the GPU (`paper_1910_11239_b200.experiment`, mirror of
   targets, converged everywhere, mesh-independent (spread <= 1), and the
   degree robustness of the MVS V-cycle.
 """
-import numpy as np
 import pytest
 
 from _common import golden_mg

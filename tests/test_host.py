@@ -9,7 +9,7 @@ import sys
 import numpy as np
 import pytest
 
-from _common import golden, have_reference, inputs, rel, REF_SRC
+from _common import golden, have_reference, rel, REF_SRC
 
 import paper_1910_11239_b200 as dg
 from paper_1910_11239_b200 import basis as B
