@@ -24,7 +24,12 @@ struct Res3Shape {
   static constexpr int G = fdm2_groups<3, N>();
   static constexpr int F = N * N;
   static constexpr int NT = G * F;
-  static constexpr int CS = 2 * L::SZ + 8 * N * N;  // A, B tensors + F1[4], F2[4] fields
+  // face fields: rows of N at an odd pitch NP (the row-wise M_0 transform
+  // reads a row per thread: a pitch of N = 8 or 16 doubles put every thread
+  // of a half-warp on the same bank, 40% of the kernel's shared wavefronts)
+  static constexpr int NP = N | 1;
+  static constexpr int FP = N * NP;                  // one face field
+  static constexpr int CS = 2 * L::SZ + 8 * FP;      // A, B tensors + F1[4], F2[4] fields
   static constexpr int SMEM = G * CS;                // doubles
   // CTAs per SM the register budget is sized for (launch_res.cu: DGB_RES3_MINB)
   static constexpr int MINB = 2;
@@ -110,7 +115,8 @@ res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
   double* A = sm + g * S::CS;
   double* B = A + L::SZ;
   double* F1 = B + L::SZ;      // F1[q][i2][i0]: faces along t = 1
-  double* F2 = F1 + 4 * F;     // F2[q][i1][i0]: faces along t = 2
+  double* F2 = F1 + 4 * S::FP;  // F2[q][i1][i0]: faces along t = 2
+  constexpr int FP = S::FP, NP = S::NP;
   const int fa = f % N, fb = f / N;
   const int64_t cb = (int64_t)(active ? cell : 0) * NE;
   auto nbr = [&](int t, int dir) -> const double* {  // neighbour cell data or null
@@ -163,7 +169,7 @@ res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
       const int gb = fa + N * N * fb;
       face_scalars<N>(p, r ? r + gb : nullptr, l ? l + gb : nullptr, N, fq);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) F1[q * F + fb * N + fa] = fq[q];
+      for (int q = 0; q < 4; ++q) F1[q * FP + fb * NP + fa] = fq[q];
     }
     asm volatile("" ::: "memory");
     // faces along t = 2 at (i0, i1) = (fa, fb): fibers stride n^2
@@ -173,14 +179,14 @@ res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
       const int gb = fa + N * fb;
       face_scalars<N>(p, r ? r + gb : nullptr, l ? l + gb : nullptr, N * N, fq);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) F2[q * F + fb * N + fa] = fq[q];
+      for (int q = 0; q < 4; ++q) F2[q * FP + fb * NP + fa] = fq[q];
     }
   }
   __syncthreads();
   // ---- M_0 along i0 of the face fields, rows F1[q][i2][.] and F2[q][i1][.]
   if (active) {
     for (int w = f; w < 8 * N; w += F) {  // in place, one thread per row
-      double* row = F1 + (w / N) * F + (w % N) * N;
+      double* row = F1 + (w / N) * FP + (w % N) * NP;
       double v[N], o[N];
 #pragma unroll
       for (int j = 0; j < N; ++j) v[j] = row[j];
@@ -194,19 +200,19 @@ res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
   double bq[N];
   if (active) {
     for (int w = f; w < 4 * N; w += F) {  // F2 column (q, i0): in place
-      double* col = F2 + (w / N) * F + (w % N);
+      double* col = F2 + (w / N) * FP + (w % N);
       double v[N], o[N];
 #pragma unroll
-      for (int j = 0; j < N; ++j) v[j] = col[j * N];
+      for (int j = 0; j < N; ++j) v[j] = col[j * NP];
       mass3<N>(p, v, o);
 #pragma unroll
-      for (int j = 0; j < N; ++j) col[j * N] = o[j];
+      for (int j = 0; j < N; ++j) col[j * NP] = o[j];
     }
     const int sb = L::sbase(1, f), ss = L::sstride(1);
     double v[N], o[N], t[N];
     double fq[4];  // faces along t = 1, transformed by M_0
 #pragma unroll
-    for (int q = 0; q < 4; ++q) fq[q] = F1[q * F + fb * N + fa];
+    for (int q = 0; q < 4; ++q) fq[q] = F1[q * FP + fb * NP + fa];
 #pragma unroll
     for (int k = 0; k < N; ++k) v[k] = B[sb + k * ss];
     res_adiag<N>(p, dig[1], v, t);  // G_1 b
@@ -233,7 +239,7 @@ res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
     double v[N], o[N], t[N];
     double fq[4];  // faces along t = 2, transformed by M_0 and M_1
 #pragma unroll
-    for (int q = 0; q < 4; ++q) fq[q] = F2[q * F + fb * N + fa];
+    for (int q = 0; q < 4; ++q) fq[q] = F2[q * FP + fb * NP + fa];
 #pragma unroll
     for (int k = 0; k < N; ++k) v[k] = B[sb + k * ss];
     res_adiag<N>(p, dig[2], v, t);  // G_2 d
