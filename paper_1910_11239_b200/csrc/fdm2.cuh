@@ -440,6 +440,32 @@ __device__ __forceinline__ void bulk_red_add(double* gdst, const void* ssrc, uns
                : "memory");
 }
 
+// Dense cell rows of 8 or 16 doubles (64 / 128 bytes) put the 16-byte
+// accesses of a quarter-warp (8 consecutive rows) into the same bank group.
+// Each thread therefore starts its row at chunk row_rot (distinct bank
+// groups across the quarter-warp) and the chunk registers are rotated with a
+// log-depth select network, so the register array stays statically indexed.
+template <int N>
+__device__ __forceinline__ int row_rot(int f) {
+  return N == 16 ? (f & 7) : ((f >> 1) & 3);  // N = 8: rows pair up in a bank group
+}
+// w[j] <- w[(j + r) % C] for 0 <= r < C (C a power of two)
+template <int C>
+__device__ __forceinline__ void rotate_chunks(double2 (&w)[C], int r) {
+#pragma unroll
+  for (int b = 1; b < C; b <<= 1) {
+    const bool on = (r & b) != 0;
+    double2 t[C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) t[j] = w[(j + b) % C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      w[j].x = on ? t[j].x : w[j].x;
+      w[j].y = on ? t[j].y : w[j].y;
+    }
+  }
+}
+
 // shared offset of cell slot s in the dense (bulk-staged) layout: the small
 // skew keeps the 16-byte row accesses of a quarter-warp that straddles two
 // cells in distinct bank groups (fits: 8 cells + 8 doubles <= tensor size)
@@ -554,11 +580,27 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         const double* src = buf + dense_off<NEc>(slot0 + h) + goff;
+        if constexpr (N % 8 == 0) {
+          // rows of 64 / 128 bytes: the quarter-warp's 16-byte accesses start
+          // in rotated chunks (distinct bank groups), registers rotated back
+          double2 w[N / 2];
+          const int rot = row_rot<N>(f);
 #pragma unroll
-        for (int i = 0; i < N; i += 2) {
-          const double2 t = *reinterpret_cast<const double2*>(src + i);
-          v[h * N + i] = t.x;
-          v[h * N + i + 1] = t.y;
+          for (int j = 0; j < N / 2; ++j)
+            w[j] = *reinterpret_cast<const double2*>(src + 2 * ((j + rot) & (N / 2 - 1)));
+          rotate_chunks<N / 2>(w, (N / 2 - rot) & (N / 2 - 1));
+#pragma unroll
+          for (int j = 0; j < N / 2; ++j) {
+            v[h * N + 2 * j] = w[j].x;
+            v[h * N + 2 * j + 1] = w[j].y;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < N; i += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(src + i);
+            v[h * N + i] = t.x;
+            v[h * N + i + 1] = t.y;
+          }
         }
       }
       fdm_matvec<M, true>(p.mats, p.eo, dg[0], v, o);
@@ -648,10 +690,23 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
 #pragma unroll
       for (int h = 0; h < H; ++h) {
         double* dst = buf + dense_off<NEc>(slot0 + h) + goff;
+        if constexpr (N % 8 == 0) {
+          double2 w[N / 2];
 #pragma unroll
-        for (int i = 0; i < N; i += 2)
-          *reinterpret_cast<double2*>(dst + i) =
-              make_double2(__dmul_rn(p.omega, o[h * N + i]), __dmul_rn(p.omega, o[h * N + i + 1]));
+          for (int j = 0; j < N / 2; ++j)
+            w[j] = make_double2(__dmul_rn(p.omega, o[h * N + 2 * j]),
+                                __dmul_rn(p.omega, o[h * N + 2 * j + 1]));
+          const int rot = row_rot<N>(f);
+          rotate_chunks<N / 2>(w, rot);
+#pragma unroll
+          for (int j = 0; j < N / 2; ++j)
+            *reinterpret_cast<double2*>(dst + 2 * ((j + rot) & (N / 2 - 1))) = w[j];
+        } else {
+#pragma unroll
+          for (int i = 0; i < N; i += 2)
+            *reinterpret_cast<double2*>(dst + i) =
+                make_double2(__dmul_rn(p.omega, o[h * N + i]), __dmul_rn(p.omega, o[h * N + i + 1]));
+        }
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -705,10 +760,19 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
 #ifndef FDM_BULK_REGS
 #define FDM_BULK_REGS 56
 #endif
+#ifndef FDM_BULK_REGS_M16
+#define FDM_BULK_REGS_M16 80
+#endif
+// (m = 16: v[16], o[16] alone are 64 registers -- 56 would spill ~350 B per
+// thread; 80 gives 3 CTAs of 256 threads without spills)
+template <int M>
+__host__ __device__ constexpr int fdm2_bulk_regs() {
+  return M >= 16 ? FDM_BULK_REGS_M16 : FDM_BULK_REGS;
+}
 template <int D, int M>
 __host__ __device__ constexpr int fdm2_min_ctas(bool bulk) {
-  return bulk ? (65536 / (fdm2_groups<D, M>() * Lay<D, M>::F * FDM_BULK_REGS) > 0
-                     ? 65536 / (fdm2_groups<D, M>() * Lay<D, M>::F * FDM_BULK_REGS)
+  return bulk ? (65536 / (fdm2_groups<D, M>() * Lay<D, M>::F * fdm2_bulk_regs<M>()) > 0
+                     ? 65536 / (fdm2_groups<D, M>() * Lay<D, M>::F * fdm2_bulk_regs<M>())
                      : 1)
               : 0;  // 0: no minimum (ptxas default heuristics)
 }
