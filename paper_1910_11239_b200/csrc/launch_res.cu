@@ -50,13 +50,16 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
       const size_t smem3 = sizeof(double) * S::SMEM;
       const unsigned grid = (unsigned)((q.count + S::G - 1) / S::G);
       const int minb = env_int("DGB_RES3_MINB", S::MINB);
-      auto k3 = minb >= 3 ? res3_kernel<N, 3> : res3_kernel<N, 2>;
+      // occupancy variants (CTAs per SM the register budget is sized for);
+      // the high counts only where the 128-thread CTAs fit them (n <= 8)
+      constexpr int HI = N <= 8 ? 8 : 3, MID = N <= 8 ? 6 : 3;
+      auto k3 = minb >= HI ? res3_kernel<N, HI>
+                           : (minb >= MID ? res3_kernel<N, MID>
+                                          : (minb >= 3 ? res3_kernel<N, 3> : res3_kernel<N, 2>));
       static bool attr3 = false;
       if (!attr3) {
-        DG_CUDA(cudaFuncSetAttribute(res3_kernel<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem3));
-        DG_CUDA(cudaFuncSetAttribute(res3_kernel<N, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem3));
+        for (auto kk : {res3_kernel<N, 2>, res3_kernel<N, 3>, res3_kernel<N, MID>, res3_kernel<N, HI>})
+          DG_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
         attr3 = true;
       }
       k3<<<grid, S::NT, smem3, st>>>(p);

@@ -31,8 +31,11 @@ struct Res3Shape {
   static constexpr int FP = N * NP;                  // one face field
   static constexpr int CS = 2 * L::SZ + 8 * FP;      // A, B tensors + F1[4], F2[4] fields
   static constexpr int SMEM = G * CS;                // doubles
-  // CTAs per SM the register budget is sized for (launch_res.cu: DGB_RES3_MINB)
-  static constexpr int MINB = 2;
+  // CTAs per SM the register budget is sized for (launch_res.cu: DGB_RES3_MINB).
+  // n = 8 (128-thread CTAs): 6 -> 80 registers, no spills (cfg 3 residual
+  // 1.35 -> 1.29 ms; 8 CTAs / 64 registers spill and lose); n = 7 (147
+  // threads) and n >= 9 keep 2 (n = 7 at 6: 0.25 -> 0.44 ms)
+  static constexpr int MINB = N == 8 ? 6 : 2;
 };
 
 // the four face scalars of a fiber along t (zero where the neighbour is absent)
