@@ -763,11 +763,11 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
 #ifndef FDM_BULK_REGS_M16
 #define FDM_BULK_REGS_M16 80
 #endif
-// (m = 16: v[16], o[16] alone are 64 registers -- 56 would spill ~350 B per
+// (m >= 14: v[m], o[m] alone are 56-64 registers -- 56 would spill ~350 B per
 // thread; 80 gives 3 CTAs of 256 threads without spills)
 template <int M>
 __host__ __device__ constexpr int fdm2_bulk_regs() {
-  return M >= 16 ? FDM_BULK_REGS_M16 : FDM_BULK_REGS;
+  return M >= 14 ? FDM_BULK_REGS_M16 : FDM_BULK_REGS;
 }
 template <int D, int M>
 __host__ __device__ constexpr int fdm2_min_ctas(bool bulk) {
