@@ -815,11 +815,12 @@ int dg_patch_gather_map(const dg_level_t* L, const int32_t* patches, int64_t cou
 
 // internal launches over the level's packed colour lists (no index division)
 static int res_packed(dg_level_t* L, const double* x, const double* b, double* r,
-                      const DevList& l, cudaStream_t st) {
+                      const DevList& l, cudaStream_t st, int block_list = 0) {
   ResArgs p = res_params(L, x, b, r);
   p.list = l.ptr;
   p.count = l.count;
   p.packed = 1;
+  p.block_list = block_list;
   return dispatch_residual(L->d, L->n, p, L->hres(), st);
 }
 
@@ -1000,7 +1001,7 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
       for (int i = 0; i < nc; ++i) {
         const int k = reverse ? nc - 1 - i : i;
         *nl += 2;
-        if ((rc = res_packed(L, x, b, r, L->pcol_cells_pk[k], st))) return rc;
+        if ((rc = res_packed(L, x, b, r, L->pcol_cells_pk[k], st, 1))) return rc;
         if ((rc = patch_fdm_packed(L, r, x, omega, L->pcol_pk[k], st))) return rc;
       }
       return DG_OK;

@@ -31,6 +31,7 @@ struct ResArgs {
   int64_t start = 0;
   int64_t count = 0;
   int packed = 0;
+  int block_list = 0;  // list = vertex-patch cells, 2x2x2 blocks of 8 in slot order
   double alpha = 0, beta = 0, betap = 0;
   Geo geo;
 };

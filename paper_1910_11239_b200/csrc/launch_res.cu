@@ -71,6 +71,10 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
   p.blocked = 0;
   p.bz0 = p.bnz = 0;
   if constexpr (D == 3 && G == 8) {
+    // vertex-patch cell lists (the MVS restricted residual): every group of
+    // 8 list entries is one patch's 2x2x2 block, in-block traces from shared
+    if (q.list && q.block_list && q.count % 8 == 0 && env_int("DGB_RES_BLOCK_LIST", 1))
+      p.blocked = 2;
     // whole layers on 2x2x2 cell blocks: half the neighbour traces come from
     // the block's own shared tensors
     const int64_t lc = (int64_t)q.geo.nc[0] * q.geo.nc[1];

@@ -43,7 +43,9 @@ struct Res2Params {
   double alpha, beta, betap;
   int packed;   // list entries are packed global cell coordinates (pack3)
   int eo;       // mass and interior stiffness on the even/odd path
-  int blocked;  // range mode on 2x2x2 cell blocks (G = 8): layers [bz0, bz0 + bnz)
+  int blocked;  // 1: range mode on 2x2x2 cell blocks (G = 8), layers [bz0, bz0 + bnz);
+                // 2: list mode whose consecutive groups of 8 cells are 2x2x2
+                //    blocks in slot order dx + 2 dy + 4 dz (vertex-patch cells)
   int bz0, bnz;
   Geo geo;
   ResMats<N> mats;
@@ -225,9 +227,10 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
   __shared__ int s_c[G][3];
   const int tid = threadIdx.x;
   constexpr bool BLK = (D == 3 && G == 8);
-  const bool blocked = BLK && p.blocked && !list;
+  const bool range_blocked = BLK && p.blocked == 1 && !list;
+  const bool blocked = range_blocked || (BLK && p.blocked == 2 && list);
   if (tid < G) {
-    if (blocked) {
+    if (range_blocked) {
       // CTA = 2x2x2 cell block; group g = dx + 2 dy + 4 dz
       const int nbx = (p.geo.nc[0] + 1) >> 1, nby = (p.geo.nc[1] + 1) >> 1;
       const int64_t bxy = (int64_t)nbx * nby;

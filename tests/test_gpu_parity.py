@@ -410,6 +410,25 @@ def test_host_pipelined_step_matches_device_step(kind, omega, k):
     assert rel(xn, OracleLevel((nc,) * 3, k).smooth(kind, omega, x0, b)) <= RTOL
 
 
+@pytest.mark.parametrize("k", [3, 5])
+def test_mvs_block_list_residual_bitwise(k, monkeypatch):
+    """The MVS restricted residual on vertex-patch cell lists runs in 2x2x2
+    block mode (in-block neighbour traces from shared memory): bitwise the
+    per-cell list mode, and at the oracle."""
+    ctx, _, sm = _setup(3, 6, k, "mvs", 1.0)
+    x0, b = inputs(ctx.ndofs, 14)
+    out = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv("DGB_RES_BLOCK_LIST", v)
+        sm.use_graph = False
+        x = x0.copy()
+        sm.smooth(x, b)
+        out[v] = x
+    assert np.array_equal(out["0"], out["1"])
+    want = OracleLevel((6,) * 3, k).smooth("mvs", 1.0, x0, b)
+    assert rel(out["1"], want) <= RTOL
+
+
 def test_local_solver_apply_inverse_is_exact_local_solve():
     """`LocalSolver.apply_inverse` (fastdiag.py:118-133) on the device: the
     cell solver inverts the Kronecker-sum cell matrix, the patch solver the
