@@ -187,6 +187,24 @@ int dg_xpby(const double* z, double beta, double* p, int64_t n, void* stream);
 int dg_dot(const double* a, const double* b, int64_t n, double* part, double* out,
            void* stream);
 
+/* SIPG operator on a multilinear (distorted) cube level, SURVEY 8(f) row 3
+ * (dgop.apply_operator / residual non-Cartesian branches, dgop.py:432-481,
+ * 583-759).  Geometry arrays are device fp64 in the reference's layouts
+ * (paper_1910_11239_b200/distorted.py builds them); tables are host arrays.
+ * out = A u, or out = b - A u when b != NULL.                               */
+typedef struct dg_dist_args {
+  int dim, degree, ncells_dim;
+  const double* metric;    /* (cells, n^d, d(d+1)/2) detJ J^-1 J^-T w        */
+  const double* faces[3];  /* per direction: (faces, n^(d-1), 1 + 2d)        */
+  const double* bnd[6];    /* per direction and side: (faces, n^(d-1), 1 + d) */
+  const double* vals;      /* host (n, n): V[q][i] = phi_i(x_q)               */
+  const double* grads;     /* host (n, n): D[q][i] = phi_i'(x_q)              */
+  const double* bv;        /* host (2, n) basis values at x = 0, 1            */
+  const double* bg;        /* host (2, n) basis derivatives at x = 0, 1       */
+} dg_dist_args_t;
+int dg_dist_apply(const dg_dist_args_t* args, const double* u, const double* b, double* out,
+                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

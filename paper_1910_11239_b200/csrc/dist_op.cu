@@ -1,0 +1,346 @@
+// dist_op.cu - SIPG operator on multilinear (distorted) cells, SURVEY 8(f)
+// row 3 (reference: dgop._volume_apply / _faces_apply non-Cartesian
+// branches, dgop.py:432-481, 583-759; geometry dgop.py:277-374).
+//
+// One CTA per cell, all tensors of the cell in shared memory:
+//  - volume: the d reference gradients at the n^d Gauss points by
+//    sum-factorised contractions (values / derivative tables per direction,
+//    shared prefixes), the symmetric metric detJ J^-1 J^-T w per point
+//    (host-precomputed), and the adjoint contractions back to the nodes;
+//  - faces: for each of the 2d faces the cell evaluates the value and the
+//    full reference gradient of itself and (interior faces) of its
+//    neighbour at the face Gauss points, forms the SIPG face moments with the
+//    per-point penalty and normal-derivative factors, and adds only its own
+//    side's contribution -- every interior face is evaluated by both of its
+//    cells, so the kernel needs no atomics and no face colouring;
+//  - out = A u, or out = b - A u.
+// Index conventions: nodes canonical (direction 1 fastest); face fields
+// [q_t2][q_t1] with t1 < t2 the transverse directions; the host geometry is
+// in the reference's reversed layouts (first direction slowest).
+#include "launch.h"
+
+namespace dgb {
+
+using DistArgs = dg_dist_args_t;  // include/dgmg_b200.h; ctypes mirror in distorted.py
+
+template <int N>
+struct DistTabs {
+  double V[N * N], Dg[N * N], bv[2][N], bg[2][N];
+};
+
+template <int D, int N>
+struct DistParams {
+  const double* u;
+  const double* b;
+  double* out;
+  const double* metric;
+  const double* faces[3];
+  const double* bnd[6];
+  int n;
+  DistTabs<N> tab;
+};
+
+// out[e] (+)= sum_j M(o, j) in[e | i_dir = j] over an N^K tensor (dir 0 fastest);
+// M(o, j) = TR ? M[j*N + o] : M[o*N + j].  Ends with a barrier.
+template <int K, int N, bool TR, bool ACC>
+__device__ __forceinline__ void contract(double* out, const double* in, int dir, const double* M) {
+  constexpr int TOT = K == 3 ? N * N * N : (K == 2 ? N * N : N);
+  const int stride = dir == 0 ? 1 : (dir == 1 ? N : N * N);
+  for (int e = threadIdx.x; e < TOT; e += blockDim.x) {
+    const int o = (e / stride) % N;
+    const int base = e - o * stride;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(TR ? M[j * N + o] : M[o * N + j], in[base + j * stride], s);
+    out[e] = ACC ? out[e] + s : s;
+  }
+  __syncthreads();
+}
+
+// canonical element index of cell-local nodes: (transverse e = i_t1 + N i_t2, i_tau)
+template <int D, int N>
+__device__ __forceinline__ int elem(int tau, int e, int i) {
+  if (D == 2) {
+    const int it = e;  // the one transverse direction
+    return tau == 1 ? i + N * it : it + N * i;
+  }
+  const int a = e % N, b = e / N;  // i_t1, i_t2 (t1 < t2)
+  if (tau == 1) return i + N * a + N * N * b;
+  if (tau == 2) return a + N * i + N * N * b;
+  return a + N * b + N * N * i;
+}
+
+// traces along tau at side p: tv = sum_i bv_p[i] X, tg = sum_i bg_p[i] X
+template <int D, int N>
+__device__ __forceinline__ void traces(const DistTabs<N>& T, const double* X, int tau, int p,
+                                       double* tv, double* tg) {
+  constexpr int FT = D == 3 ? N * N : N;
+  for (int e = threadIdx.x; e < FT; e += blockDim.x) {
+    double sv = 0.0, sg = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double x = X[elem<D, N>(tau, e, i)];
+      sv = fma(T.bv[p][i], x, sv);
+      sg = fma(T.bg[p][i], x, sg);
+    }
+    tv[e] = sv;
+    tg[e] = sg;
+  }
+  __syncthreads();
+}
+
+// value and the d reference gradients at the face points from the traces;
+// G[t] for t = 0..D-1 (direction t+1): normal for t+1 == tau
+template <int D, int N>
+__device__ __forceinline__ void face_values(const DistTabs<N>& T, const double* tv,
+                                            const double* tg, int tau, double* val, double* G0,
+                                            double* G1, double* G2, double* tmp) {
+  double* G[3] = {G0, G1, G2};
+  if (D == 2) {
+    const int tt = tau == 1 ? 1 : 0;  // transverse direction index (0-based)
+    contract<1, N, false, false>(val, tv, 0, T.V);
+    contract<1, N, false, false>(G[tt], tv, 0, T.Dg);
+    contract<1, N, false, false>(G[tau - 1], tg, 0, T.V);
+    return;
+  }
+  const int t1 = tau == 1 ? 1 : 0, t2 = tau == 3 ? 1 : 2;  // 0-based transverse dirs
+  contract<2, N, false, false>(tmp, tv, 0, T.V);           // V along t1
+  contract<2, N, false, false>(val, tmp, 1, T.V);          // V along t2
+  contract<2, N, false, false>(G[t2], tmp, 1, T.Dg);       // d/d t2
+  contract<2, N, false, false>(tmp, tv, 0, T.Dg);          // D along t1
+  contract<2, N, false, false>(G[t1], tmp, 1, T.V);        // d/d t1
+  contract<2, N, false, false>(tmp, tg, 0, T.V);
+  contract<2, N, false, false>(G[tau - 1], tmp, 1, T.V);   // normal
+}
+
+// adjoint: acc[node] += bv_p (x) (V^T V^T val + tangential adjoints of M_t)
+//                     + bg_p (x) V^T V^T M_tau
+template <int D, int N>
+__device__ __forceinline__ void face_scatter(const DistTabs<N>& T, double* acc, int tau, int p,
+                                             double* mval, double* M0, double* M1, double* M2,
+                                             double* tv, double* tg, double* tmp) {
+  double* Mm[3] = {M0, M1, M2};
+  constexpr int FT = D == 3 ? N * N : N;
+  if (D == 2) {
+    const int tt = tau == 1 ? 1 : 0;
+    contract<1, N, true, false>(tv, mval, 0, T.V);
+    contract<1, N, true, true>(tv, Mm[tt], 0, T.Dg);
+    contract<1, N, true, false>(tg, Mm[tau - 1], 0, T.V);
+  } else {
+    const int t1 = tau == 1 ? 1 : 0, t2 = tau == 3 ? 1 : 2;
+    // tv = V1^T V2^T mval + V1^T D2^T M_t2 + D1^T V2^T M_t1;  tg = V1^T V2^T M_tau
+    contract<2, N, true, false>(tmp, mval, 1, T.V);
+    contract<2, N, true, true>(tmp, Mm[t2], 1, T.Dg);
+    contract<2, N, true, false>(tv, tmp, 0, T.V);
+    contract<2, N, true, false>(tmp, Mm[t1], 1, T.V);
+    contract<2, N, true, true>(tv, tmp, 0, T.Dg);
+    contract<2, N, true, false>(tmp, Mm[tau - 1], 1, T.V);
+    contract<2, N, true, false>(tg, tmp, 0, T.V);
+  }
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  for (int x = threadIdx.x; x < ND; x += blockDim.x) {
+    // decompose x into (transverse e, i_tau)
+    int i, e;
+    if (D == 2) {
+      const int i1 = x % N, i2 = x / N;
+      i = tau == 1 ? i1 : i2;
+      e = tau == 1 ? i2 : i1;
+    } else {
+      const int i1 = x % N, i2 = (x / N) % N, i3 = x / (N * N);
+      if (tau == 1) { i = i1; e = i2 + N * i3; }
+      else if (tau == 2) { i = i2; e = i1 + N * i3; }
+      else { i = i3; e = i1 + N * i2; }
+    }
+    acc[x] += T.bv[p][i] * tv[e] + T.bg[p][i] * tg[e];
+  }
+  (void)FT;
+  __syncthreads();
+}
+
+template <int D, int N>
+__global__ void __launch_bounds__(128) dist_apply_kernel(const __grid_constant__ DistParams<D, N> P) {
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  constexpr int FT = D == 3 ? N * N : N;
+  constexpr int S = D == 3 ? 6 : 3;
+  extern __shared__ __align__(16) double sm[];
+  double* U = sm;
+  double* NB = U + ND;
+  double* A = NB + ND;
+  double* B = A + ND;
+  double* C = B + ND;
+  double* E = C + ND;
+  double* F = E + ND;
+  double* fs = F + ND;  // face scratch: 20 fields of FT
+  const int n = P.n;
+  const int64_t cell = blockIdx.x;
+  int c[3];
+  {
+    int64_t r = cell;
+    for (int t = 0; t < D; ++t) {
+      c[t] = (int)(r % n);
+      r /= n;
+    }
+  }
+  const DistTabs<N>& T = P.tab;
+  for (int e = threadIdx.x; e < ND; e += blockDim.x) U[e] = P.u[cell * ND + e];
+  __syncthreads();
+  // ---------------- volume
+  const double* G = P.metric + cell * (int64_t)ND * S;
+  if (D == 3) {
+    contract<3, N, false, false>(A, U, 0, T.V);
+    contract<3, N, false, false>(B, U, 0, T.Dg);
+    contract<3, N, false, false>(C, A, 1, T.V);    // x12vv
+    contract<3, N, false, false>(E, B, 1, T.V);    // x12dv
+    contract<3, N, false, false>(F, A, 1, T.Dg);   // x12vd
+    contract<3, N, false, false>(A, E, 2, T.V);    // g1
+    contract<3, N, false, false>(B, F, 2, T.V);    // g2
+    contract<3, N, false, false>(E, C, 2, T.Dg);   // g3
+    for (int e = threadIdx.x; e < ND; e += blockDim.x) {
+      const int q1 = e % N, q2 = (e / N) % N, q3 = e / (N * N);
+      const double* g = G + (int64_t)(q1 * N * N + q2 * N + q3) * S;  // reversed index
+      const double a1 = A[e], a2 = B[e], a3 = E[e];
+      A[e] = g[0] * a1 + g[3] * a2 + g[4] * a3;
+      B[e] = g[3] * a1 + g[1] * a2 + g[5] * a3;
+      E[e] = g[4] * a1 + g[5] * a2 + g[2] * a3;
+    }
+    __syncthreads();
+    contract<3, N, true, false>(C, A, 2, T.V);     // s3_1
+    contract<3, N, true, false>(F, B, 2, T.V);     // s3_2
+    contract<3, N, true, false>(A, E, 2, T.Dg);    // s3_3
+    contract<3, N, true, false>(B, C, 1, T.V);     // s2_1
+    contract<3, N, true, false>(E, F, 1, T.Dg);    // s2_23 = D^T s3_2
+    contract<3, N, true, true>(E, A, 1, T.V);      //        + V^T s3_3
+    contract<3, N, true, false>(C, B, 0, T.Dg);
+    contract<3, N, true, true>(C, E, 0, T.V);
+  } else {
+    contract<2, N, false, false>(A, U, 0, T.V);    // x1v
+    contract<2, N, false, false>(B, U, 0, T.Dg);   // x1d
+    contract<2, N, false, false>(E, B, 1, T.V);    // g1
+    contract<2, N, false, false>(F, A, 1, T.Dg);   // g2
+    for (int e = threadIdx.x; e < ND; e += blockDim.x) {
+      const int q1 = e % N, q2 = e / N;
+      const double* g = G + (int64_t)(q1 * N + q2) * S;
+      const double a1 = E[e], a2 = F[e];
+      E[e] = g[0] * a1 + g[2] * a2;
+      F[e] = g[2] * a1 + g[1] * a2;
+    }
+    __syncthreads();
+    contract<2, N, true, false>(A, E, 1, T.V);
+    contract<2, N, true, false>(B, F, 1, T.Dg);
+    contract<2, N, true, false>(C, A, 0, T.Dg);
+    contract<2, N, true, true>(C, B, 0, T.V);
+  }
+  // ---------------- faces
+  double* tvo = fs;            double* tgo = fs + FT;
+  double* tvn = fs + 2 * FT;   double* tgn = fs + 3 * FT;
+  double* vo = fs + 4 * FT;    double* go[3] = {fs + 5 * FT, fs + 6 * FT, fs + 7 * FT};
+  double* vn = fs + 8 * FT;    double* gn[3] = {fs + 9 * FT, fs + 10 * FT, fs + 11 * FT};
+  double* mv = fs + 12 * FT;   double* mm[3] = {fs + 13 * FT, fs + 14 * FT, fs + 15 * FT};
+  double* tmp = fs + 16 * FT;  double* sv = fs + 17 * FT;  double* sg = fs + 18 * FT;
+  for (int tau = 1; tau <= D; ++tau) {
+    const int t0 = tau - 1;
+    for (int p = 0; p < 2; ++p) {
+      const bool boundary = p == 0 ? c[t0] == 0 : c[t0] == n - 1;
+      traces<D, N>(T, U, tau, p, tvo, tgo);
+      face_values<D, N>(T, tvo, tgo, tau, vo, go[0], go[1], go[2], tmp);
+      // face index in the reference's slab order (first direction slowest)
+      int64_t f = 0;
+      if (boundary) {
+        for (int t = D - 1; t >= 0; --t)
+          if (t != t0) f = f * n + c[t];
+      } else {
+        int lc[3] = {c[0], c[1], c[2]};
+        if (p == 0) lc[t0] -= 1;  // own is the right cell
+        for (int t = D - 1; t >= 0; --t) f = f * (t == t0 ? n - 1 : n) + lc[t];
+        int nb[3] = {c[0], c[1], c[2]};
+        nb[t0] += p == 1 ? 1 : -1;
+        int64_t nid = 0;
+        for (int t = D - 1; t >= 0; --t) nid = nid * n + nb[t];
+        for (int e = threadIdx.x; e < ND; e += blockDim.x) NB[e] = P.u[nid * ND + e];
+        __syncthreads();
+        traces<D, N>(T, NB, tau, 1 - p, tvn, tgn);
+        face_values<D, N>(T, tvn, tgn, tau, vn, gn[0], gn[1], gn[2], tmp);
+      }
+      // face moments at the points, own side only
+      for (int e = threadIdx.x; e < FT; e += blockDim.x) {
+        int gi;  // reversed face-point index: first transverse direction slowest
+        if (D == 3) gi = (e % N) * N + e / N;
+        else gi = e;
+        if (boundary) {
+          const double* g = P.bnd[2 * t0 + p] + (f * FT + gi) * (1 + D);
+          double m = vo[e] * g[0];
+          for (int t = 0; t < D; ++t) m -= go[t][e] * g[1 + t];
+          mv[e] = m;
+          for (int t = 0; t < D; ++t) mm[t][e] = -vo[e] * g[1 + t];
+        } else {
+          const double* g = P.faces[t0] + (f * FT + gi) * (1 + 2 * D);
+          const bool left = p == 1;
+          const double vp = left ? vo[e] : vn[e], vmn = left ? vn[e] : vo[e];
+          const double jump = vp - vmn;
+          double m = jump * g[0];
+          for (int t = 0; t < D; ++t) {
+            const double gp = left ? go[t][e] : gn[t][e];
+            const double gm = left ? gn[t][e] : go[t][e];
+            m -= gp * g[1 + t] + gm * g[1 + D + t];
+          }
+          mv[e] = left ? m : -m;
+          for (int t = 0; t < D; ++t) mm[t][e] = -jump * g[(left ? 1 : 1 + D) + t];
+        }
+      }
+      __syncthreads();
+      face_scatter<D, N>(T, C, tau, p, mv, mm[0], mm[1], mm[2], sv, sg, tmp);
+    }
+  }
+  for (int e = threadIdx.x; e < ND; e += blockDim.x)
+    P.out[cell * ND + e] = P.b ? P.b[cell * ND + e] - C[e] : C[e];
+}
+
+template <int D, int N>
+static int launch_dist(const DistArgs& a, const double* u, const double* b, double* out,
+                       cudaStream_t st) {
+  DistParams<D, N> P;
+  P.u = u;
+  P.b = b;
+  P.out = out;
+  P.metric = a.metric;
+  for (int t = 0; t < 3; ++t) P.faces[t] = a.faces[t];
+  for (int t = 0; t < 6; ++t) P.bnd[t] = a.bnd[t];
+  P.n = a.ncells_dim;
+  for (int q = 0; q < N * N; ++q) {
+    P.tab.V[q] = a.vals[q];
+    P.tab.Dg[q] = a.grads[q];
+  }
+  for (int p = 0; p < 2; ++p)
+    for (int i = 0; i < N; ++i) {
+      P.tab.bv[p][i] = a.bv[p * N + i];
+      P.tab.bg[p][i] = a.bg[p * N + i];
+    }
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  constexpr int FT = D == 3 ? N * N : N;
+  const size_t smem = sizeof(double) * (7 * (size_t)ND + 20 * (size_t)FT);
+  auto k = dist_apply_kernel<D, N>;
+  if (smem > 48 * 1024)
+    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t ncells = 1;
+  for (int t = 0; t < D; ++t) ncells *= a.ncells_dim;
+  k<<<(unsigned)ncells, 128, smem, st>>>(P);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
+}  // namespace dgb
+
+extern "C" int dg_dist_apply(const dg_dist_args_t* args, const double* u, const double* b,
+                             double* out, void* stream) {
+  using namespace dgb;
+  if (!args || !u || !out) return fail(DG_EINVAL, "null argument");
+  const DistArgs& a = *args;
+  const int n = a.degree + 1;
+  cudaStream_t st = (cudaStream_t)stream;
+#define DG_DCASE(D, NN) \
+  if (a.dim == D && n == NN) return launch_dist<D, NN>(a, u, b, out, st);
+  DG_DCASE(2, 2) DG_DCASE(2, 3) DG_DCASE(2, 4) DG_DCASE(2, 5) DG_DCASE(2, 6) DG_DCASE(2, 7)
+  DG_DCASE(2, 8) DG_DCASE(3, 2) DG_DCASE(3, 3) DG_DCASE(3, 4) DG_DCASE(3, 5) DG_DCASE(3, 6)
+#undef DG_DCASE
+  return fail(DG_EUNSUPPORTED, "distorted operator: dim 2 (k <= 7) or 3 (k <= 5)");
+}
