@@ -204,6 +204,13 @@ typedef struct dg_dist_args {
 } dg_dist_args_t;
 int dg_dist_apply(const dg_dist_args_t* args, const double* u, const double* b, double* out,
                   void* stream);
+/* Surrogate cell solves on a multilinear level (CellSolverSet per-cell
+ * batch, fastdiag.py:381-436, 457-496): x_c += omega Z Lambda_c^-1 Z^T r_c
+ * with per-cell eigenbases z (dim, ncells, n, n) and 1/Lambda-sums inv
+ * (ncells, n^dim, reversed layout), all device; cells NULL = every cell.    */
+int dg_dist_cell_fdm(int dim, int degree, int64_t ncells, const double* z, const double* inv,
+                     const double* r, double* x, double omega, const int32_t* cells,
+                     int64_t n_cells, void* stream);
 
 #ifdef __cplusplus
 }

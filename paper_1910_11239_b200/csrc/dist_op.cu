@@ -295,6 +295,43 @@ __global__ void __launch_bounds__(128) dist_apply_kernel(const __grid_constant__
     P.out[cell * ND + e] = P.b ? P.b[cell * ND + e] - C[e] : C[e];
 }
 
+// Surrogate cell solves on multilinear levels (fastdiag.py:381-436, 457-496):
+// x_c += omega (Z_d x .. x Z_1) diag(1/Lambda_c) (Z_d^T x .. x Z_1^T) r_c with
+// per-cell 1D eigenbases Z_t (global memory, staged per CTA in shared).
+template <int D, int N>
+__global__ void __launch_bounds__(128)
+    dist_cell_fdm_kernel(const double* __restrict__ r, double* __restrict__ x,
+                         const double* __restrict__ Z, const double* __restrict__ inv,
+                         const int32_t* __restrict__ list, int64_t ncells, double omega) {
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  __shared__ double T0[ND], T1[ND], Zs[3][N * N];
+  const int64_t cell = list ? list[blockIdx.x] : blockIdx.x;
+  for (int t = 0; t < D; ++t)
+    for (int e = threadIdx.x; e < N * N; e += blockDim.x)
+      Zs[t][e] = Z[((int64_t)t * ncells + cell) * N * N + e];
+  for (int e = threadIdx.x; e < ND; e += blockDim.x) T0[e] = r[cell * ND + e];
+  __syncthreads();
+  double* a = T0;
+  double* b = T1;
+  for (int t = 0; t < D; ++t) {  // forward: Z^T along each direction
+    contract<D, N, true, false>(b, a, t, Zs[t]);
+    double* s = a; a = b; b = s;
+  }
+  for (int e = threadIdx.x; e < ND; e += blockDim.x) {  // 1/Lambda, reversed index
+    int ri;
+    if (D == 3) ri = (e % N) * N * N + ((e / N) % N) * N + e / (N * N);
+    else ri = (e % N) * N + e / N;
+    a[e] *= inv[cell * ND + ri];
+  }
+  __syncthreads();
+  for (int t = D - 1; t >= 0; --t) {  // backward: Z along each direction
+    contract<D, N, false, false>(b, a, t, Zs[t]);
+    double* s = a; a = b; b = s;
+  }
+  for (int e = threadIdx.x; e < ND; e += blockDim.x)
+    x[cell * ND + e] = fma(omega, a[e], x[cell * ND + e]);
+}
+
 template <int D, int N>
 static int launch_dist(const DistArgs& a, const double* u, const double* b, double* out,
                        cudaStream_t st) {
@@ -343,4 +380,27 @@ extern "C" int dg_dist_apply(const dg_dist_args_t* args, const double* u, const 
   DG_DCASE(2, 8) DG_DCASE(3, 2) DG_DCASE(3, 3) DG_DCASE(3, 4) DG_DCASE(3, 5) DG_DCASE(3, 6)
 #undef DG_DCASE
   return fail(DG_EUNSUPPORTED, "distorted operator: dim 2 (k <= 7) or 3 (k <= 5)");
+}
+
+extern "C" int dg_dist_cell_fdm(int dim, int degree, int64_t ncells, const double* z,
+                                const double* inv, const double* r, double* x, double omega,
+                                const int32_t* cells, int64_t n_cells, void* stream) {
+  using namespace dgb;
+  if (!z || !inv || !r || !x || (cells && n_cells < 0)) return fail(DG_EINVAL, "bad argument");
+  if (r == x) return fail(DG_EINVAL, "cell solve: r must not alias x");
+  const int n = degree + 1;
+  const int64_t nb = cells ? n_cells : ncells;
+  if (nb == 0) return DG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+#define DG_FCASE(D, NN)                                                                     \
+  if (dim == D && n == NN) {                                                               \
+    dist_cell_fdm_kernel<D, NN><<<(unsigned)nb, 128, 0, st>>>(r, x, z, inv, cells, ncells, \
+                                                               omega);                     \
+    DG_CUDA(cudaGetLastError());                                                           \
+    return DG_OK;                                                                          \
+  }
+  DG_FCASE(2, 2) DG_FCASE(2, 3) DG_FCASE(2, 4) DG_FCASE(2, 5) DG_FCASE(2, 6) DG_FCASE(2, 7)
+  DG_FCASE(2, 8) DG_FCASE(3, 2) DG_FCASE(3, 3) DG_FCASE(3, 4) DG_FCASE(3, 5) DG_FCASE(3, 6)
+#undef DG_FCASE
+  return fail(DG_EUNSUPPORTED, "surrogate cell solve: dim 2 (k <= 7) or 3 (k <= 5)");
 }

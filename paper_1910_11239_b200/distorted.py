@@ -17,10 +17,15 @@ Mirror of the reference's non-Cartesian path:
   cell, sum-factorised reference gradients at the quadrature points, the
   metric applied per point, the adjoint contractions; every face term is
   evaluated by both of its cells (each adds its own side), so there are no
-  atomics (`dgop.py:432-481`, `583-759`, non-Cartesian branches).
-
-The surrogate cell smoother on these meshes (`fastdiag.py:381-436`) is the
-next step; it is not built yet.
+  atomics (`dgop.py:432-481`, `583-759`, non-Cartesian branches);
+- `SurrogateCellSolverSet` (`fastdiag.py:381-436`, `457-496`): per cell and
+  direction the 1D SIPG pencil of the cell's surrogate box (edge-averaged
+  lengths, `mesh.py:436-458`), eigenpairs batched on the host (the north
+  star keeps the 1D eigenproblems there), the per-cell fast-diagonalisation
+  solves on the device (`dist_cell_fdm_kernel`);
+- `DistortedSmoother` (ACS / MCS, `smoothers.py:131-166`; vertex patches
+  need Cartesian geometry in the reference too), `compute_rhs`
+  (`dgop.py:800-871`, multilinear branch) and the hooks the V-cycle uses.
 """
 
 from __future__ import annotations
@@ -35,7 +40,8 @@ from ._device import Staged, require_cuda, stream_handle
 from .basis import Basis1D, sipg_penalty
 
 __all__ = ["DistortedLevel", "DistortedHierarchy", "distort", "DistortedContext",
-           "make_distorted_context", "apply_operator", "residual"]
+           "make_distorted_context", "apply_operator", "residual", "surrogate_lengths",
+           "SurrogateCellSolverSet", "DistortedSmoother", "compute_rhs", "assemble_dense"]
 
 _SYM = {2: [(0, 0), (1, 1), (0, 1)], 3: [(0, 0), (1, 1), (2, 2), (0, 1), (0, 2), (1, 2)]}
 
@@ -210,6 +216,8 @@ class DistortedGeometry:
         if np.any(det <= 0.0):
             raise ValueError("nonpositive Jacobian at a quadrature point")
         adj = _adjugate(jac)
+        self.detjw = det * wq
+        self.ref = ref
         g = np.einsum("fqxt,fqxs->fqts", adj, adj)
         self.metric = np.empty(det.shape + (len(_SYM[d]),))
         for j_, (a, b) in enumerate(_SYM[d]):
@@ -281,9 +289,12 @@ class DistortedContext:
             raise NotImplementedError("distorted device operator: dim 2 or 3")
         if basis.qpts.size != basis.n:
             raise NotImplementedError("distorted device operator: n_q = k + 1 quadrature")
+        from .dgop import DofLayout
         self.level, self.basis, self.gamma_hat = level, basis, gamma_hat
         self.dim, self.n = level.dim, basis.n
         self.ndofs = level.ncells * basis.n ** level.dim
+        self.layout = DofLayout(dim=level.dim, degree=basis.degree, dims=tuple(level.dims))
+        self.counter = None
         self.geom = DistortedGeometry(level, basis, gamma_hat)
         self._dev = None
 
@@ -363,3 +374,218 @@ def residual(ctx: DistortedContext, x, b, out):
     _lib.check(lib.dg_dist_apply(ctypes.byref(a), sx.ptr, sb.ptr, so.ptr, stream_handle()))
     so.finish()
     return out
+
+
+def assemble_dense(ctx: DistortedContext, device="cuda") -> torch.Tensor:
+    """Dense level matrix from device operator applications (coarse levels)."""
+    n = ctx.ndofs
+    if n > 40000:
+        raise ValueError("dense assembly limited to 40000 dofs")
+    eye = torch.eye(n, dtype=torch.float64, device="cuda")
+    a = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    for j in range(n):
+        apply_operator(ctx, eye[j], out=a[j])
+    return a.T.contiguous().to(device)
+
+
+# ------------------------------------------------------------ cell smoother
+def surrogate_lengths(corners: np.ndarray) -> np.ndarray:
+    """Per direction the mean length of the 2^(d-1) edges aligned with it."""
+    d = corners.shape[-1]
+    out = np.empty(corners.shape[:-2] + (d,))
+    for t in range(d):
+        ls = [np.linalg.norm(corners[..., c + (1 << t), :] - corners[..., c, :], axis=-1)
+              for c in range(2 ** d) if not (c >> t) & 1]
+        st = np.stack(ls, axis=-1)
+        if np.any(st <= 0.0):
+            raise ValueError("degenerate (zero-length) edge")
+        out[..., t] = st.mean(axis=-1)
+    return out
+
+
+def _batched_geneig(a: np.ndarray, m: np.ndarray):
+    """Z^T A Z = diag(lam), Z^T M Z = I for stacks (B, n, n) (Cholesky
+    reduction + symmetric eigensolve, host)."""
+    chol = np.linalg.cholesky(m)
+    c = np.linalg.solve(chol, a)
+    c = np.linalg.solve(chol, c.transpose(0, 2, 1))
+    c = 0.5 * (c + c.transpose(0, 2, 1))
+    lam, v = np.linalg.eigh(c)
+    return np.linalg.solve(chol.transpose(0, 2, 1), v), lam
+
+
+class SurrogateCellSolverSet:
+    """Per-cell surrogate fast-diagonalisation solvers (`fastdiag.py:381-436`)."""
+
+    kind = "cell"
+
+    def __init__(self, ctx: DistortedContext):
+        from .fastdiag import SingularLocalSolverError
+        lvl, b = ctx.level, ctx.basis
+        d, n, nn, k = lvl.dim, lvl.ncells_dim, b.n, b.degree
+        self.ctx, self.dim, self.n1 = ctx, d, nn
+        hbar = surrogate_lengths(lvl.cell_corners())
+        B = lvl.ncells
+        w = np.asarray(b.qwts, float)
+        mref = (b.values * w) @ b.values.T
+        lref = (b.grads * w) @ b.grads.T
+        bv, bg = b.bv, b.bg
+        zs, lams = [], []
+        for t in range(d):
+            pos = (np.arange(B) // n ** t) % n
+            h = hbar[:, t]
+            ge = ctx.gamma_hat * k * (k + 1) * (2.0 / h)
+            eta = (np.where(pos == 0, 1.0, 0.5), np.where(pos == n - 1, 1.0, 0.5))
+            a = lref[None] / h[:, None, None]
+            for p in (0, 1):
+                g1 = (-1.0 if p == 0 else 1.0) * np.outer(bv[p], bg[p])
+                a = a + (ge * eta[p])[:, None, None] * np.outer(bv[p], bv[p])[None] \
+                    - (eta[p] / h)[:, None, None] * (g1 + g1.T)[None]
+            z, lam = _batched_geneig(a, h[:, None, None] * mref[None])
+            zs.append(z)
+            lams.append(lam)
+        inv = None
+        for t in range(d):
+            shape = [B] + [1] * d
+            shape[1 + t] = nn
+            arr = lams[t].reshape(shape)
+            inv = arr if inv is None else inv + arr
+        if np.any(inv <= 0.0):
+            raise SingularLocalSolverError("nonpositive Kronecker-sum eigenvalue")
+        dev = torch.device("cuda")
+        self._z = torch.from_numpy(np.ascontiguousarray(np.stack(zs))).to(dev)
+        self._inv = torch.from_numpy(np.ascontiguousarray((1.0 / inv).reshape(B, -1))).to(dev)
+        self.ncells = B
+
+    def solve_partitioned(self, x, r, parts, omega: float) -> None:
+        """x[cells] += omega A_c^-1 r_c for the given cell ids (None = all)."""
+        lib = _lib.load()
+        n = self.ctx.ndofs
+        sx, sr = Staged(x, n, "x"), Staged(r, n, "r")
+        ids = None
+        cnt = 0
+        if parts is not None:
+            ids = torch.as_tensor(np.asarray(parts, dtype=np.int32)).cuda()
+            cnt = int(ids.numel())
+            if cnt == 0:
+                sx.finish()
+                return
+        _lib.check(lib.dg_dist_cell_fdm(self.dim, self.n1 - 1, self.ncells, self._z.data_ptr(),
+                                        self._inv.data_ptr(), sr.ptr, sx.ptr, float(omega),
+                                        None if ids is None else ids.data_ptr(), cnt,
+                                        stream_handle()))
+        sx.finish()
+
+
+class DistortedSmoother:
+    """ACS / MCS smoothing steps on a multilinear level (`smoothers.py:131-166`)."""
+
+    def __init__(self, ctx: DistortedContext, config):
+        if config.kind not in ("acs", "mcs"):
+            raise ValueError("vertex-patch smoothers require Cartesian geometry")
+        self.ctx, self.config = ctx, config
+        self.set = SurrogateCellSolverSet(ctx)
+        n = ctx.level.ncells_dim
+        ids = np.arange(ctx.level.ncells)
+        par = np.zeros(ctx.level.ncells, dtype=np.int64)
+        rem = ids.copy()
+        for _ in range(ctx.dim):
+            par += rem % n
+            rem //= n
+        self.colors = [ids] if config.kind == "acs" else \
+            [s for s in (ids[par % 2 == 0], ids[par % 2 == 1]) if len(s)]
+        self._parts = [None] if config.kind == "acs" else \
+            [torch.as_tensor(c.astype(np.int32)).cuda() for c in self.colors]
+        self.all_parts = None
+        self._r = torch.empty(ctx.ndofs, dtype=torch.float64, device="cuda")
+        self.use_graph = False
+
+    def _solve(self, x, part, omega):
+        lib = _lib.load()
+        s = self.set
+        cnt = 0 if part is None else int(part.numel())
+        _lib.check(lib.dg_dist_cell_fdm(s.dim, s.n1 - 1, s.ncells, s._z.data_ptr(),
+                                        s._inv.data_ptr(), self._r.data_ptr(), x.data_ptr(),
+                                        float(omega), None if part is None else part.data_ptr(),
+                                        cnt, stream_handle()))
+
+    def smooth(self, x, b, reverse: bool = False) -> None:
+        n = self.ctx.ndofs
+        sx, sb = Staged(x, n, "x"), Staged(b, n, "b")
+        om = self.config.omega
+        if self.config.kind == "acs":
+            residual(self.ctx, sx.dev, sb.dev, self._r)
+            self._solve(sx.dev, None, om)
+        else:
+            order = range(len(self._parts))
+            for c in (reversed(order) if reverse else order):
+                residual(self.ctx, sx.dev, sb.dev, self._r)
+                self._solve(sx.dev, self._parts[c], om)
+        sx.finish()
+
+
+# ---------------------------------------------------------------- load vector
+def _corner_values(d: int, ref: np.ndarray) -> np.ndarray:
+    out = np.ones((2 ** d, ref.shape[0]))
+    for c in range(2 ** d):
+        for t in range(d):
+            x = ref[:, t]
+            out[c] = out[c] * (x if (c >> t) & 1 else 1.0 - x)
+    return out
+
+
+def compute_rhs(ctx: DistortedContext, f, g) -> np.ndarray:
+    """Load vector on a multilinear level (`dgop.py:800-871`): source f at the
+    mapped Gauss points times detJ w, Nitsche boundary terms of g with the
+    boundary penalty and the full normal-derivative factors; the basis
+    contractions run on the device."""
+    from .dgop import _contract_quad
+    lvl, b, geo = ctx.level, ctx.basis, ctx.geom
+    d, n, nn = lvl.dim, lvl.ncells_dim, b.n
+    pts = np.asarray(b.qpts, float)
+    dev = torch.device("cuda")
+    vals = torch.from_numpy(np.ascontiguousarray(b.values)).to(dev)   # (n, nq)
+    grads = torch.from_numpy(np.ascontiguousarray(b.grads)).to(dev)
+    corners = lvl.cell_corners()
+    coords = np.einsum("fcx,cq->fqx", corners, _corner_values(d, geo.ref))
+    fv = np.asarray(f(coords.reshape(-1, d)), dtype=float).reshape(lvl.ncells, -1) * geo.detjw
+    w = torch.from_numpy(fv).to(dev).reshape((lvl.ncells,) + (nn,) * d)
+    rhs = _contract_quad(w, vals, d).reshape(lvl.ncells, -1)
+    cidx = np.indices((n,) * d).reshape(d, -1)[::-1].T                  # (ncells, d), v_1 first
+    bv = torch.from_numpy(np.asarray(b.bv, float)).to(dev)
+    bg = torch.from_numpy(np.asarray(b.bg, float)).to(dev)
+    for tau in range(1, d + 1):
+        trans = [t for t in range(1, d + 1) if t != tau]
+        tp = _tensor_points(pts, d - 1)
+        for p in (0, 1):
+            ids = np.nonzero(cidx[:, tau - 1] == (0 if p == 0 else n - 1))[0]
+            fref = np.empty((tp.shape[0], d))
+            for j_, t in enumerate(trans):
+                fref[:, t - 1] = tp[:, j_]
+            fref[:, tau - 1] = float(p)
+            fc = np.einsum("fcx,cq->fqx", corners[ids], _corner_values(d, fref))
+            gv = np.asarray(g(fc.reshape(-1, d)), dtype=float).reshape(len(ids), -1)
+            pack = geo.bnd[tau - 1][p]                                     # (Fb, qf, 1 + d)
+            mv = torch.from_numpy(gv * pack[..., 0]).to(dev)
+            mom = [torch.from_numpy(-gv * pack[..., 1 + t]).to(dev) for t in range(d)]
+            k_ = len(trans)
+            nf = len(ids)
+            if k_ == 0:
+                tv, tg = mv.reshape(nf), mom[tau - 1].reshape(nf)
+            else:
+                shp = (nf,) + (nn,) * k_
+                tv = _contract_quad(mv.reshape(shp), vals, k_)
+                for j_, t in enumerate(trans):
+                    # tangential moment: derivative table along t, values elsewhere
+                    y = mom[t - 1].reshape(shp)
+                    for a_ in range(k_):
+                        y = torch.tensordot(y, grads if a_ == j_ else vals, dims=([1], [1]))
+                    tv = tv + (y.permute(0, *range(k_, 0, -1)) if k_ > 1 else y)
+                tg = _contract_quad(mom[tau - 1].reshape(shp), vals, k_)
+            tv = tv.reshape((nf,) + (nn,) * k_)
+            tg = tg.reshape((nf,) + (nn,) * k_)
+            ax = 1 + (d - tau)
+            shape = [1] * ax + [nn] + [1] * (d - ax)
+            contrib = tv.unsqueeze(ax) * bv[p].reshape(shape) + tg.unsqueeze(ax) * bg[p].reshape(shape)
+            rhs[torch.from_numpy(ids).to(dev)] += contrib.reshape(nf, -1)
+    return rhs.reshape(-1).cpu().numpy()

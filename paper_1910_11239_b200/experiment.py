@@ -7,8 +7,9 @@ rules (`bench.py:93-167`), and `run_experiment` — right-hand side, V-cycle
 preconditioner, CG or GMRES to a relative residual reduction, one record per
 level (`bench.py:190-300`).  Every vector lives on the device: the load
 vector (`dgop.compute_rhs`), the V-cycle (`multigrid.VCycle`) and the Krylov
-iteration (`krylov.pcg` / `krylov.pgmres`).  Only Cartesian meshes are in
-scope (distorted meshes are SURVEY 8(f) row 3).
+iteration (`krylov.pcg` / `krylov.pgmres`).  Distorted meshes
+(`mesh_kind="distorted"`) run the multilinear operator,
+load vector and surrogate cell smoothers of `distorted.py`.
 """
 
 from __future__ import annotations
@@ -72,19 +73,23 @@ def manufactured(dim: int) -> ManufacturedProblem:
     return ManufacturedProblem(dim=dim, sigma=SIGMA, points=BELL_CENTRES_3D[:, :dim].copy())
 
 
-_OMEGA = {"acs": 0.7, "mcs": 1.0, "avs": 0.25, "mvs": 1.0}  # Cartesian (bench.py:93-102)
+_OMEGA = {("acs", "cartesian"): 0.7, ("mcs", "cartesian"): 1.0, ("avs", "cartesian"): 0.25,
+          ("mvs", "cartesian"): 1.0, ("acs", "distorted"): 0.5, ("mcs", "distorted"): 0.75,
+          ("avs", "distorted"): 0.25, ("mvs", "distorted"): 1.0}  # bench.py:93-102
 
 
 @dataclass
 class ExperimentConfig:
-    """`bench.py:105-167` (Cartesian meshes)."""
+    """`bench.py:105-167`."""
 
     dim: int = 2
     degree: int = 3
     coarse_cells: int | None = None
     level_min: int = 3
     level_max: int = 3
-    mesh_kind: str = "cartesian"
+    mesh_kind: str = "cartesian"       # "cartesian" | "distorted"
+    distortion: float = 0.25
+    seed: int = 1234
     gamma_hat: float | None = None
     smoother: str = "acs"
     omega: float | None = None
@@ -100,27 +105,30 @@ class ExperimentConfig:
         cfg = replace(self)
         if cfg.dim not in (2, 3):
             raise ValueError("dim must be 2 or 3")
-        if cfg.mesh_kind != "cartesian":
-            raise NotImplementedError("distorted meshes are not part of the device path")
-        if cfg.smoother not in _OMEGA:
+        if cfg.mesh_kind not in ("cartesian", "distorted"):
+            raise ValueError("mesh must be cartesian or distorted")
+        if cfg.smoother not in ("acs", "mcs", "avs", "mvs"):
             raise ValueError("smoother must be one of acs, mcs, avs, mvs")
         if cfg.level_min > cfg.level_max or cfg.level_min < 0:
             raise ValueError("invalid level range")
+        dist = cfg.mesh_kind == "distorted"
         if cfg.coarse_cells is None:
-            cfg.coarse_cells = 2
+            cfg.coarse_cells = 2 if not dist else (32 if cfg.dim == 2 else 8)
         if cfg.gamma_hat is None:
-            cfg.gamma_hat = 1.0
+            cfg.gamma_hat = 1.0 if not dist else 4.0
         if cfg.omega is None:
-            cfg.omega = _OMEGA[cfg.smoother]
+            cfg.omega = _OMEGA[(cfg.smoother, cfg.mesh_kind)]
         multiplicative = cfg.smoother in ("mcs", "mvs")
         if cfg.solver is None:
-            cfg.solver = "gmres" if multiplicative else "cg"
+            cfg.solver = "gmres" if multiplicative and not dist else "cg"
         if cfg.solver not in ("cg", "gmres"):
             raise ValueError("solver must be cg or gmres")
         if cfg.symmetrize is None:
             cfg.symmetrize = bool(multiplicative and cfg.solver == "cg")
         if multiplicative and cfg.solver == "cg" and not cfg.symmetrize:
             raise ValueError("multiplicative smoothing inside CG requires the symmetrized V-cycle")
+        if dist and cfg.smoother in ("avs", "mvs"):
+            raise ValueError("vertex-patch smoothers are not supported on distorted meshes")
         return cfg
 
 
@@ -144,15 +152,23 @@ def _run_level(cfg: ExperimentConfig, level: int, problem: ManufacturedProblem) 
     t0 = time.perf_counter()
     hier = mesh.build_hierarchy(cfg.dim, cfg.coarse_cells, level)
     basis = Basis1D.make(cfg.degree)
-    ctxs = [dgop.make_context(lvl, basis, gamma_hat=cfg.gamma_hat) for lvl in hier.levels]
+    dist = cfg.mesh_kind == "distorted"
+    if dist:
+        from . import distorted
+        hier = distorted.distort(hier, cfg.distortion, cfg.seed)
+        ctxs = [distorted.DistortedContext(lvl, basis, cfg.gamma_hat) for lvl in hier.levels]
+    else:
+        ctxs = [dgop.make_context(lvl, basis, gamma_hat=cfg.gamma_hat) for lvl in hier.levels]
     sm = SmootherConfig(kind=cfg.smoother, omega=cfg.omega, m_pre=cfg.m_pre,
                         m_post=cfg.m_post, symmetrize=cfg.symmetrize)
     cycle = VCycle(ctxs, basis, MultigridConfig(smoother=sm, coarse=cfg.coarse_solver))
     ctx = ctxs[-1]
-    b = torch.from_numpy(dgop.compute_rhs(ctx, problem.f, problem.g)).cuda()
+    rhs_fn = distorted.compute_rhs if dist else dgop.compute_rhs
+    apply_fn = distorted.apply_operator if dist else dgop.apply_operator
+    b = torch.from_numpy(rhs_fn(ctx, problem.f, problem.g)).cuda()
 
     def op(x, out):
-        dgop.apply_operator(ctx, x, out=out)
+        apply_fn(ctx, x, out=out)
 
     def pre(r, out):
         cycle.apply(r, out)

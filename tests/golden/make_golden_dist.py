@@ -38,6 +38,37 @@ def main() -> None:
         out[name + "/grid"] = lvl.vertex_grid.copy()
         out[name + "/Au"] = dgop.apply_operator(ctx, u)
         out[name + "/meta"] = np.array([d, coarse, level, k])
+    # surrogate cell solver set, smoothing steps, load vector (fastdiag.py:381-496,
+    # smoothers.py:131-166, dgop.py:800-871) on the 2D k = 3 and 3D k = 2 meshes
+    from dgmg import fastdiag as fd
+    from dgmg.smoothers import SmootherConfig, make_level_smoother
+    from dgmg.bench import ExperimentConfig, manufactured, run_experiment
+    for name, d, coarse, level, k in (("dsm_2d_k3", 2, 2, 2, 3), ("dsm_3d_k2", 3, 2, 1, 2)):
+        hier = mesh.distort(mesh.build_hierarchy(d, coarse, level), 0.25, rng_seed=2024)
+        lvl = hier.levels[level]
+        basis = Basis1D.make(k)
+        ctx = dgop.make_context(lvl, basis, gamma_hat=4.0)
+        r = np.random.default_rng(5).uniform(-1.0, 1.0, ctx.ndofs)
+        x = np.zeros(ctx.ndofs)
+        fd.CellSolverSet(lvl, basis, 4.0).solve_scaled_into(x, r, None, 0.5)
+        out[name + "/cellset"] = x
+        b = np.random.default_rng(6).uniform(-1.0, 1.0, ctx.ndofs)
+        for kind, om in (("acs", 0.5), ("mcs", 0.75)):
+            sm = make_level_smoother(ctx, basis, SmootherConfig(kind=kind, omega=om))
+            x = np.random.default_rng(7).uniform(-1.0, 1.0, ctx.ndofs)
+            sm.smooth(x, b)
+            out[name + f"/{kind}"] = x
+        prob = manufactured(d)
+        out[name + "/rhs"] = dgop.compute_rhs(ctx, prob.f, prob.g)
+        out[name + "/meta"] = np.array([d, coarse, level, k])
+    for name, d, k, coarse, l0, l1, sm_kind in (("dex_acs_2d_k2", 2, 2, 4, 1, 2, "acs"),
+                                                ("dex_mcs_2d_k2", 2, 2, 4, 1, 1, "mcs"),
+                                                ("dex_acs_3d_k2", 3, 2, 2, 1, 1, "acs")):
+        recs = run_experiment(ExperimentConfig(dim=d, degree=k, coarse_cells=coarse,
+                                               level_min=l0, level_max=l1, smoother=sm_kind,
+                                               mesh_kind="distorted", max_it=120))
+        out[name + "/records"] = np.array([[r.level, r.iterations, r.nu_frac, float(r.converged)]
+                                           for r in recs])
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT}: {len(out)} arrays")
 

@@ -16,7 +16,9 @@ from paper_1910_11239_b200.basis import Basis1D
 pytestmark = pytest.mark.gpu
 G = dict(np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
                               "golden_dist.npz")))
-CASES = sorted({k.split("/")[0] for k in G})
+CASES = sorted({k.split("/")[0] for k in G if k.startswith("dop_")})
+SMS = sorted({k.split("/")[0] for k in G if k.startswith("dsm_")})
+EXS = sorted({k.split("/")[0] for k in G if k.startswith("dex_")})
 
 
 def _ctx(name):
@@ -47,3 +49,54 @@ def test_distorted_operator_symmetric(name):
     s1, s2 = float(v @ au), float(u @ av)
     assert abs(s1 - s2) <= 1e-12 * max(1.0, abs(s1))
     assert float(u @ au) > 0.0
+
+
+def _sm_ctx(name):
+    d, coarse, level, k = (int(v) for v in G[name + "/meta"])
+    h = D.distort(mesh.build_hierarchy(d, coarse, level), 0.25, 2024)
+    return D.DistortedContext(h.levels[level], Basis1D.make(k), 4.0)
+
+
+@pytest.mark.parametrize("name", SMS)
+def test_surrogate_cell_solves_and_steps_match_reference(name):
+    """Surrogate cell solver set (`fastdiag.py:381-496`) and the ACS / MCS
+    smoothing steps on the distorted mesh against the reference's."""
+    from paper_1910_11239_b200.smoothers import SmootherConfig
+    ctx = _sm_ctx(name)
+    n = ctx.ndofs
+    r = np.random.default_rng(5).uniform(-1.0, 1.0, n)
+    x = np.zeros(n)
+    D.SurrogateCellSolverSet(ctx).solve_partitioned(x, r, None, 0.5)
+    assert rel(x, G[name + "/cellset"]) <= RTOL
+    b = np.random.default_rng(6).uniform(-1.0, 1.0, n)
+    for kind, om in (("acs", 0.5), ("mcs", 0.75)):
+        sm = D.DistortedSmoother(ctx, SmootherConfig(kind=kind, omega=om))
+        x = np.random.default_rng(7).uniform(-1.0, 1.0, n)
+        sm.smooth(x, b)
+        assert rel(x, G[name + f"/{kind}"]) <= RTOL
+
+
+@pytest.mark.parametrize("name", SMS)
+def test_distorted_compute_rhs_matches_reference(name):
+    from paper_1910_11239_b200.experiment import manufactured
+    ctx = _sm_ctx(name)
+    prob = manufactured(ctx.dim)
+    assert rel(D.compute_rhs(ctx, prob.f, prob.g), G[name + "/rhs"]) <= 1e-13
+
+
+@pytest.mark.parametrize("name", EXS)
+def test_distorted_solver_runs_match_reference(name):
+    """`run_experiment(mesh_kind="distorted")`: V-cycle with surrogate cell
+    smoothers, dense coarse solve, CG: the reference's iteration counts."""
+    from paper_1910_11239_b200.experiment import ExperimentConfig, run_experiment
+    _, smoother, dd, kk = name.split("_")
+    d, k = int(dd[0]), int(kk[1:])
+    ref = G[name + "/records"]
+    coarse = 4 if d == 2 else 2
+    recs = run_experiment(ExperimentConfig(dim=d, degree=k, coarse_cells=coarse,
+                                           level_min=int(ref[0, 0]), level_max=int(ref[-1, 0]),
+                                           smoother=smoother, mesh_kind="distorted", max_it=120))
+    for r, (lv, it, nu, conv) in zip(recs, ref):
+        assert r.level == int(lv) and r.converged == bool(conv)
+        assert r.iterations == int(it)
+        assert abs(r.nu_frac - nu) <= 1e-6
