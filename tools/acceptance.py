@@ -32,3 +32,17 @@ for key, d, k, l0, l1 in RUNS:
                           "iterations": r.iterations, "nu_frac": round(r.nu_frac, 3),
                           "reference_target": TARGETS.get(key), "converged": r.converged,
                           "wall_s": round(r.wall_time, 3)}), flush=True)
+
+# criterion 6: distorted meshes (test_acceptance.py:187-220)
+for key, lv0, lv1, sm, om, m, target in (("dist_acs1_2d_k3", 3, 5, "acs", 0.5, 1, {3: 38.7, 4: 37.6, 5: 37.6}),
+                                         ("dist_mcs1_2d_k3", 4, 4, "mcs", 0.75, 1, {4: 23.5}),
+                                         ("dist_acs2_2d_k3", 3, 3, "acs", 0.5, 2, {})):
+    for r in run_experiment(ExperimentConfig(dim=2, degree=3, level_min=lv0, level_max=lv1,
+                                             smoother=sm, mesh_kind="distorted", omega=om,
+                                             m_pre=m, m_post=m, max_it=120)):
+        print(json.dumps({"run": key, "level": r.level, "coarse_cells": 32,
+                          "cells_per_dim": 32 * 2 ** r.level, "dofs": r.dofs,
+                          "solver": r.config["solver"], "iterations": r.iterations,
+                          "nu_frac": round(r.nu_frac, 3),
+                          "reference_target": target.get(r.level), "converged": r.converged,
+                          "wall_s": round(r.wall_time, 3)}), flush=True)
