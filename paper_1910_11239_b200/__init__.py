@@ -6,7 +6,7 @@ the additive / coloured-multiplicative smoothing steps, computed by
 hand-written sm_100a CUDA kernels behind a C ABI (include/dgmg_b200.h).
 """
 
-from . import basis, dgop, fastdiag, flops, krylov, mesh, multigrid, smoothers, tables  # noqa: F401
+from . import basis, dgop, distorted, experiment, fastdiag, flops, krylov, mesh, multigrid, smoothers, tables  # noqa: F401
 from .basis import Basis1D  # noqa: F401
 from .dgop import apply_operator, make_context, residual  # noqa: F401
 from .fastdiag import CellSolverSet, PatchSolverSet, SingularLocalSolverError  # noqa: F401
