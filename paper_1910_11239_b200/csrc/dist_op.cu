@@ -40,11 +40,11 @@ struct DistParams {
   DistTabs<N> tab;
 };
 
-// out[e] (+)= sum_j M(o, j) in[e | i_dir = j] over an N^K tensor (dir 0 fastest);
-// M(o, j) = TR ? M[j*N + o] : M[o*N + j].  Ends with a barrier.
-template <int K, int N, bool TR, bool ACC>
+// out[e] (+)= sum_j M(o, j) in[e | i_dir = j] over G consecutive N^K tensors
+// (dir 0 fastest); M(o, j) = TR ? M[j*N + o] : M[o*N + j].  Ends with a barrier.
+template <int K, int N, bool TR, bool ACC, int G = 1>
 __device__ __forceinline__ void contract(double* out, const double* in, int dir, const double* M) {
-  constexpr int TOT = K == 3 ? N * N * N : (K == 2 ? N * N : N);
+  constexpr int TOT = G * (K == 3 ? N * N * N : (K == 2 ? N * N : N));
   const int stride = dir == 0 ? 1 : (dir == 1 ? N : N * N);
   for (int e = threadIdx.x; e < TOT; e += blockDim.x) {
     const int o = (e / stride) % N;
@@ -70,52 +70,54 @@ __device__ __forceinline__ int elem(int tau, int e, int i) {
   return a + N * b + N * N * i;
 }
 
-// traces along tau at side p: tv = sum_i bv_p[i] X, tg = sum_i bg_p[i] X
-template <int D, int N>
+// traces along tau at side p of G cells: tv = sum_i bv_p[i] X, tg = sum_i bg_p[i] X
+template <int D, int N, int G>
 __device__ __forceinline__ void traces(const DistTabs<N>& T, const double* X, int tau, int p,
                                        double* tv, double* tg) {
   constexpr int FT = D == 3 ? N * N : N;
-  for (int e = threadIdx.x; e < FT; e += blockDim.x) {
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  for (int x = threadIdx.x; x < G * FT; x += blockDim.x) {
+    const int g = x / FT, e = x - g * FT;
     double sv = 0.0, sg = 0.0;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const double x = X[elem<D, N>(tau, e, i)];
-      sv = fma(T.bv[p][i], x, sv);
-      sg = fma(T.bg[p][i], x, sg);
+      const double v = X[g * ND + elem<D, N>(tau, e, i)];
+      sv = fma(T.bv[p][i], v, sv);
+      sg = fma(T.bg[p][i], v, sg);
     }
-    tv[e] = sv;
-    tg[e] = sg;
+    tv[x] = sv;
+    tg[x] = sg;
   }
   __syncthreads();
 }
 
 // value and the d reference gradients at the face points from the traces;
 // G[t] for t = 0..D-1 (direction t+1): normal for t+1 == tau
-template <int D, int N>
+template <int D, int N, int G>
 __device__ __forceinline__ void face_values(const DistTabs<N>& T, const double* tv,
                                             const double* tg, int tau, double* val, double* G0,
                                             double* G1, double* G2, double* tmp) {
-  double* G[3] = {G0, G1, G2};
+  double* Gd[3] = {G0, G1, G2};
   if (D == 2) {
     const int tt = tau == 1 ? 1 : 0;  // transverse direction index (0-based)
-    contract<1, N, false, false>(val, tv, 0, T.V);
-    contract<1, N, false, false>(G[tt], tv, 0, T.Dg);
-    contract<1, N, false, false>(G[tau - 1], tg, 0, T.V);
+    contract<1, N, false, false, G>(val, tv, 0, T.V);
+    contract<1, N, false, false, G>(Gd[tt], tv, 0, T.Dg);
+    contract<1, N, false, false, G>(Gd[tau - 1], tg, 0, T.V);
     return;
   }
   const int t1 = tau == 1 ? 1 : 0, t2 = tau == 3 ? 1 : 2;  // 0-based transverse dirs
-  contract<2, N, false, false>(tmp, tv, 0, T.V);           // V along t1
-  contract<2, N, false, false>(val, tmp, 1, T.V);          // V along t2
-  contract<2, N, false, false>(G[t2], tmp, 1, T.Dg);       // d/d t2
-  contract<2, N, false, false>(tmp, tv, 0, T.Dg);          // D along t1
-  contract<2, N, false, false>(G[t1], tmp, 1, T.V);        // d/d t1
-  contract<2, N, false, false>(tmp, tg, 0, T.V);
-  contract<2, N, false, false>(G[tau - 1], tmp, 1, T.V);   // normal
+  contract<2, N, false, false, G>(tmp, tv, 0, T.V);         // V along t1
+  contract<2, N, false, false, G>(val, tmp, 1, T.V);        // V along t2
+  contract<2, N, false, false, G>(Gd[t2], tmp, 1, T.Dg);    // d/d t2
+  contract<2, N, false, false, G>(tmp, tv, 0, T.Dg);        // D along t1
+  contract<2, N, false, false, G>(Gd[t1], tmp, 1, T.V);     // d/d t1
+  contract<2, N, false, false, G>(tmp, tg, 0, T.V);
+  contract<2, N, false, false, G>(Gd[tau - 1], tmp, 1, T.V);  // normal
 }
 
 // adjoint: acc[node] += bv_p (x) (V^T V^T val + tangential adjoints of M_t)
 //                     + bg_p (x) V^T V^T M_tau
-template <int D, int N>
+template <int D, int N, int G>
 __device__ __forceinline__ void face_scatter(const DistTabs<N>& T, double* acc, int tau, int p,
                                              double* mval, double* M0, double* M1, double* M2,
                                              double* tv, double* tg, double* tmp) {
@@ -123,24 +125,24 @@ __device__ __forceinline__ void face_scatter(const DistTabs<N>& T, double* acc, 
   constexpr int FT = D == 3 ? N * N : N;
   if (D == 2) {
     const int tt = tau == 1 ? 1 : 0;
-    contract<1, N, true, false>(tv, mval, 0, T.V);
-    contract<1, N, true, true>(tv, Mm[tt], 0, T.Dg);
-    contract<1, N, true, false>(tg, Mm[tau - 1], 0, T.V);
+    contract<1, N, true, false, G>(tv, mval, 0, T.V);
+    contract<1, N, true, true, G>(tv, Mm[tt], 0, T.Dg);
+    contract<1, N, true, false, G>(tg, Mm[tau - 1], 0, T.V);
   } else {
     const int t1 = tau == 1 ? 1 : 0, t2 = tau == 3 ? 1 : 2;
     // tv = V1^T V2^T mval + V1^T D2^T M_t2 + D1^T V2^T M_t1;  tg = V1^T V2^T M_tau
-    contract<2, N, true, false>(tmp, mval, 1, T.V);
-    contract<2, N, true, true>(tmp, Mm[t2], 1, T.Dg);
-    contract<2, N, true, false>(tv, tmp, 0, T.V);
-    contract<2, N, true, false>(tmp, Mm[t1], 1, T.V);
-    contract<2, N, true, true>(tv, tmp, 0, T.Dg);
-    contract<2, N, true, false>(tmp, Mm[tau - 1], 1, T.V);
-    contract<2, N, true, false>(tg, tmp, 0, T.V);
+    contract<2, N, true, false, G>(tmp, mval, 1, T.V);
+    contract<2, N, true, true, G>(tmp, Mm[t2], 1, T.Dg);
+    contract<2, N, true, false, G>(tv, tmp, 0, T.V);
+    contract<2, N, true, false, G>(tmp, Mm[t1], 1, T.V);
+    contract<2, N, true, true, G>(tv, tmp, 0, T.Dg);
+    contract<2, N, true, false, G>(tmp, Mm[tau - 1], 1, T.V);
+    contract<2, N, true, false, G>(tg, tmp, 0, T.V);
   }
   constexpr int ND = D == 3 ? N * N * N : N * N;
-  for (int x = threadIdx.x; x < ND; x += blockDim.x) {
-    // decompose x into (transverse e, i_tau)
-    int i, e;
+  for (int xx = threadIdx.x; xx < G * ND; xx += blockDim.x) {
+    const int g = xx / ND, x = xx - g * ND;
+    int i, e;  // decompose x into (transverse e, i_tau)
     if (D == 2) {
       const int i1 = x % N, i2 = x / N;
       i = tau == 1 ? i1 : i2;
@@ -151,148 +153,175 @@ __device__ __forceinline__ void face_scatter(const DistTabs<N>& T, double* acc, 
       else if (tau == 2) { i = i2; e = i1 + N * i3; }
       else { i = i3; e = i1 + N * i2; }
     }
-    acc[x] += T.bv[p][i] * tv[e] + T.bg[p][i] * tg[e];
+    acc[xx] += T.bv[p][i] * tv[g * FT + e] + T.bg[p][i] * tg[g * FT + e];
   }
-  (void)FT;
   __syncthreads();
 }
 
+// cells per CTA: a few small cells share the 128 threads
 template <int D, int N>
-__global__ void __launch_bounds__(128) dist_apply_kernel(const __grid_constant__ DistParams<D, N> P) {
+__host__ __device__ constexpr int dist_cells() {
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  return ND >= 64 ? 1 : (128 / ND > 8 ? 8 : 128 / ND);
+}
+
+template <int D, int N>
+__global__ void __launch_bounds__(128) dist_apply_kernel(const __grid_constant__ DistParams<D, N> P,
+                                                         int64_t ncells) {
+  constexpr int G = dist_cells<D, N>();
   constexpr int ND = D == 3 ? N * N * N : N * N;
   constexpr int FT = D == 3 ? N * N : N;
   constexpr int S = D == 3 ? 6 : 3;
   extern __shared__ __align__(16) double sm[];
   double* U = sm;
-  double* NB = U + ND;
-  double* A = NB + ND;
-  double* B = A + ND;
-  double* C = B + ND;
-  double* E = C + ND;
-  double* F = E + ND;
-  double* fs = F + ND;  // face scratch: 20 fields of FT
+  double* NB = U + G * ND;
+  double* A = NB + G * ND;
+  double* B = A + G * ND;
+  double* C = B + G * ND;
+  double* E = C + G * ND;
+  double* F = E + G * ND;
+  double* fs = F + G * ND;  // face scratch: 19 fields of G * FT
+  __shared__ int s_c[G][3];
+  __shared__ int s_ok[G];
   const int n = P.n;
-  const int64_t cell = blockIdx.x;
-  int c[3];
-  {
-    int64_t r = cell;
-    for (int t = 0; t < D; ++t) {
-      c[t] = (int)(r % n);
+  const int64_t cell0 = (int64_t)blockIdx.x * G;
+  if (threadIdx.x < G) {
+    const int64_t cell = cell0 + threadIdx.x;
+    s_ok[threadIdx.x] = cell < ncells;
+    int64_t r = cell < ncells ? cell : 0;
+    for (int t = 0; t < 3; ++t) {
+      s_c[threadIdx.x][t] = t < D ? (int)(r % n) : 0;
       r /= n;
     }
   }
   const DistTabs<N>& T = P.tab;
-  for (int e = threadIdx.x; e < ND; e += blockDim.x) U[e] = P.u[cell * ND + e];
+  for (int x = threadIdx.x; x < G * ND; x += blockDim.x) {
+    const int64_t cell = cell0 + x / ND;
+    U[x] = cell < ncells ? P.u[cell * ND + x % ND] : 0.0;
+  }
   __syncthreads();
   // ---------------- volume
-  const double* G = P.metric + cell * (int64_t)ND * S;
   if (D == 3) {
-    contract<3, N, false, false>(A, U, 0, T.V);
-    contract<3, N, false, false>(B, U, 0, T.Dg);
-    contract<3, N, false, false>(C, A, 1, T.V);    // x12vv
-    contract<3, N, false, false>(E, B, 1, T.V);    // x12dv
-    contract<3, N, false, false>(F, A, 1, T.Dg);   // x12vd
-    contract<3, N, false, false>(A, E, 2, T.V);    // g1
-    contract<3, N, false, false>(B, F, 2, T.V);    // g2
-    contract<3, N, false, false>(E, C, 2, T.Dg);   // g3
-    for (int e = threadIdx.x; e < ND; e += blockDim.x) {
+    contract<3, N, false, false, G>(A, U, 0, T.V);
+    contract<3, N, false, false, G>(B, U, 0, T.Dg);
+    contract<3, N, false, false, G>(C, A, 1, T.V);    // x12vv
+    contract<3, N, false, false, G>(E, B, 1, T.V);    // x12dv
+    contract<3, N, false, false, G>(F, A, 1, T.Dg);   // x12vd
+    contract<3, N, false, false, G>(A, E, 2, T.V);    // g1
+    contract<3, N, false, false, G>(B, F, 2, T.V);    // g2
+    contract<3, N, false, false, G>(E, C, 2, T.Dg);   // g3
+    for (int x = threadIdx.x; x < G * ND; x += blockDim.x) {
+      const int g = x / ND, e = x - g * ND;
       const int q1 = e % N, q2 = (e / N) % N, q3 = e / (N * N);
-      const double* g = G + (int64_t)(q1 * N * N + q2 * N + q3) * S;  // reversed index
-      const double a1 = A[e], a2 = B[e], a3 = E[e];
-      A[e] = g[0] * a1 + g[3] * a2 + g[4] * a3;
-      B[e] = g[3] * a1 + g[1] * a2 + g[5] * a3;
-      E[e] = g[4] * a1 + g[5] * a2 + g[2] * a3;
+      const int64_t cell = s_ok[g] ? cell0 + g : 0;
+      const double* gm = P.metric + (cell * ND + q1 * N * N + q2 * N + q3) * S;  // reversed
+      const double a1 = A[x], a2 = B[x], a3 = E[x];
+      A[x] = gm[0] * a1 + gm[3] * a2 + gm[4] * a3;
+      B[x] = gm[3] * a1 + gm[1] * a2 + gm[5] * a3;
+      E[x] = gm[4] * a1 + gm[5] * a2 + gm[2] * a3;
     }
     __syncthreads();
-    contract<3, N, true, false>(C, A, 2, T.V);     // s3_1
-    contract<3, N, true, false>(F, B, 2, T.V);     // s3_2
-    contract<3, N, true, false>(A, E, 2, T.Dg);    // s3_3
-    contract<3, N, true, false>(B, C, 1, T.V);     // s2_1
-    contract<3, N, true, false>(E, F, 1, T.Dg);    // s2_23 = D^T s3_2
-    contract<3, N, true, true>(E, A, 1, T.V);      //        + V^T s3_3
-    contract<3, N, true, false>(C, B, 0, T.Dg);
-    contract<3, N, true, true>(C, E, 0, T.V);
+    contract<3, N, true, false, G>(C, A, 2, T.V);     // s3_1
+    contract<3, N, true, false, G>(F, B, 2, T.V);     // s3_2
+    contract<3, N, true, false, G>(A, E, 2, T.Dg);    // s3_3
+    contract<3, N, true, false, G>(B, C, 1, T.V);     // s2_1
+    contract<3, N, true, false, G>(E, F, 1, T.Dg);    // s2_23 = D^T s3_2
+    contract<3, N, true, true, G>(E, A, 1, T.V);      //        + V^T s3_3
+    contract<3, N, true, false, G>(C, B, 0, T.Dg);
+    contract<3, N, true, true, G>(C, E, 0, T.V);
   } else {
-    contract<2, N, false, false>(A, U, 0, T.V);    // x1v
-    contract<2, N, false, false>(B, U, 0, T.Dg);   // x1d
-    contract<2, N, false, false>(E, B, 1, T.V);    // g1
-    contract<2, N, false, false>(F, A, 1, T.Dg);   // g2
-    for (int e = threadIdx.x; e < ND; e += blockDim.x) {
+    contract<2, N, false, false, G>(A, U, 0, T.V);    // x1v
+    contract<2, N, false, false, G>(B, U, 0, T.Dg);   // x1d
+    contract<2, N, false, false, G>(E, B, 1, T.V);    // g1
+    contract<2, N, false, false, G>(F, A, 1, T.Dg);   // g2
+    for (int x = threadIdx.x; x < G * ND; x += blockDim.x) {
+      const int g = x / ND, e = x - g * ND;
       const int q1 = e % N, q2 = e / N;
-      const double* g = G + (int64_t)(q1 * N + q2) * S;
-      const double a1 = E[e], a2 = F[e];
-      E[e] = g[0] * a1 + g[2] * a2;
-      F[e] = g[2] * a1 + g[1] * a2;
+      const int64_t cell = s_ok[g] ? cell0 + g : 0;
+      const double* gm = P.metric + (cell * ND + q1 * N + q2) * S;
+      const double a1 = E[x], a2 = F[x];
+      E[x] = gm[0] * a1 + gm[2] * a2;
+      F[x] = gm[2] * a1 + gm[1] * a2;
     }
     __syncthreads();
-    contract<2, N, true, false>(A, E, 1, T.V);
-    contract<2, N, true, false>(B, F, 1, T.Dg);
-    contract<2, N, true, false>(C, A, 0, T.Dg);
-    contract<2, N, true, true>(C, B, 0, T.V);
+    contract<2, N, true, false, G>(A, E, 1, T.V);
+    contract<2, N, true, false, G>(B, F, 1, T.Dg);
+    contract<2, N, true, false, G>(C, A, 0, T.Dg);
+    contract<2, N, true, true, G>(C, B, 0, T.V);
   }
   // ---------------- faces
-  double* tvo = fs;            double* tgo = fs + FT;
-  double* tvn = fs + 2 * FT;   double* tgn = fs + 3 * FT;
-  double* vo = fs + 4 * FT;    double* go[3] = {fs + 5 * FT, fs + 6 * FT, fs + 7 * FT};
-  double* vn = fs + 8 * FT;    double* gn[3] = {fs + 9 * FT, fs + 10 * FT, fs + 11 * FT};
-  double* mv = fs + 12 * FT;   double* mm[3] = {fs + 13 * FT, fs + 14 * FT, fs + 15 * FT};
-  double* tmp = fs + 16 * FT;  double* sv = fs + 17 * FT;  double* sg = fs + 18 * FT;
+  constexpr int GF = G * FT;
+  double* tvo = fs;            double* tgo = fs + GF;
+  double* tvn = fs + 2 * GF;   double* tgn = fs + 3 * GF;
+  double* vo = fs + 4 * GF;    double* go[3] = {fs + 5 * GF, fs + 6 * GF, fs + 7 * GF};
+  double* vn = fs + 8 * GF;    double* gn[3] = {fs + 9 * GF, fs + 10 * GF, fs + 11 * GF};
+  double* mv = fs + 12 * GF;   double* mm[3] = {fs + 13 * GF, fs + 14 * GF, fs + 15 * GF};
+  double* tmp = fs + 16 * GF;  double* sv = fs + 17 * GF;  double* sg = fs + 18 * GF;
   for (int tau = 1; tau <= D; ++tau) {
     const int t0 = tau - 1;
     for (int p = 0; p < 2; ++p) {
-      const bool boundary = p == 0 ? c[t0] == 0 : c[t0] == n - 1;
-      traces<D, N>(T, U, tau, p, tvo, tgo);
-      face_values<D, N>(T, tvo, tgo, tau, vo, go[0], go[1], go[2], tmp);
-      // face index in the reference's slab order (first direction slowest)
-      int64_t f = 0;
-      if (boundary) {
-        for (int t = D - 1; t >= 0; --t)
-          if (t != t0) f = f * n + c[t];
-      } else {
-        int lc[3] = {c[0], c[1], c[2]};
-        if (p == 0) lc[t0] -= 1;  // own is the right cell
-        for (int t = D - 1; t >= 0; --t) f = f * (t == t0 ? n - 1 : n) + lc[t];
-        int nb[3] = {c[0], c[1], c[2]};
-        nb[t0] += p == 1 ? 1 : -1;
-        int64_t nid = 0;
-        for (int t = D - 1; t >= 0; --t) nid = nid * n + nb[t];
-        for (int e = threadIdx.x; e < ND; e += blockDim.x) NB[e] = P.u[nid * ND + e];
-        __syncthreads();
-        traces<D, N>(T, NB, tau, 1 - p, tvn, tgn);
-        face_values<D, N>(T, tvn, tgn, tau, vn, gn[0], gn[1], gn[2], tmp);
+      traces<D, N, G>(T, U, tau, p, tvo, tgo);
+      face_values<D, N, G>(T, tvo, tgo, tau, vo, go[0], go[1], go[2], tmp);
+      // neighbours across this face (zeros where the face is on the boundary)
+      for (int x = threadIdx.x; x < G * ND; x += blockDim.x) {
+        const int g = x / ND;
+        const int* c = s_c[g];
+        const bool bnd = !s_ok[g] || (p == 0 ? c[t0] == 0 : c[t0] == n - 1);
+        double v = 0.0;
+        if (!bnd) {
+          int64_t nid = 0;
+          for (int t = D - 1; t >= 0; --t) nid = nid * n + c[t] + (t == t0 ? (p == 1 ? 1 : -1) : 0);
+          v = P.u[nid * ND + x % ND];
+        }
+        NB[x] = v;
       }
+      __syncthreads();
+      traces<D, N, G>(T, NB, tau, 1 - p, tvn, tgn);
+      face_values<D, N, G>(T, tvn, tgn, tau, vn, gn[0], gn[1], gn[2], tmp);
       // face moments at the points, own side only
-      for (int e = threadIdx.x; e < FT; e += blockDim.x) {
-        int gi;  // reversed face-point index: first transverse direction slowest
-        if (D == 3) gi = (e % N) * N + e / N;
-        else gi = e;
+      for (int x = threadIdx.x; x < GF; x += blockDim.x) {
+        const int g = x / FT, e = x - g * FT;
+        const int* c = s_c[g];
+        const bool boundary = p == 0 ? c[t0] == 0 : c[t0] == n - 1;
+        const int gi = D == 3 ? (e % N) * N + e / N : e;  // reversed face-point index
+        int64_t f = 0;  // face index in the reference's slab order (first direction slowest)
         if (boundary) {
-          const double* g = P.bnd[2 * t0 + p] + (f * FT + gi) * (1 + D);
-          double m = vo[e] * g[0];
-          for (int t = 0; t < D; ++t) m -= go[t][e] * g[1 + t];
-          mv[e] = m;
-          for (int t = 0; t < D; ++t) mm[t][e] = -vo[e] * g[1 + t];
+          for (int t = D - 1; t >= 0; --t)
+            if (t != t0) f = f * n + c[t];
+          const double* gg = P.bnd[2 * t0 + p] + (f * FT + gi) * (1 + D);
+          double m = vo[x] * gg[0];
+          for (int t = 0; t < D; ++t) m -= go[t][x] * gg[1 + t];
+          mv[x] = s_ok[g] ? m : 0.0;
+          for (int t = 0; t < D; ++t) mm[t][x] = s_ok[g] ? -vo[x] * gg[1 + t] : 0.0;
         } else {
-          const double* g = P.faces[t0] + (f * FT + gi) * (1 + 2 * D);
+          for (int t = D - 1; t >= 0; --t)
+            f = f * (t == t0 ? n - 1 : n) + c[t] - (t == t0 && p == 0 ? 1 : 0);
+          const double* gg = P.faces[t0] + (f * FT + gi) * (1 + 2 * D);
           const bool left = p == 1;
-          const double vp = left ? vo[e] : vn[e], vmn = left ? vn[e] : vo[e];
+          const double vp = left ? vo[x] : vn[x], vmn = left ? vn[x] : vo[x];
           const double jump = vp - vmn;
-          double m = jump * g[0];
+          double m = jump * gg[0];
           for (int t = 0; t < D; ++t) {
-            const double gp = left ? go[t][e] : gn[t][e];
-            const double gm = left ? gn[t][e] : go[t][e];
-            m -= gp * g[1 + t] + gm * g[1 + D + t];
+            const double gp = left ? go[t][x] : gn[t][x];
+            const double gm = left ? gn[t][x] : go[t][x];
+            m -= gp * gg[1 + t] + gm * gg[1 + D + t];
           }
-          mv[e] = left ? m : -m;
-          for (int t = 0; t < D; ++t) mm[t][e] = -jump * g[(left ? 1 : 1 + D) + t];
+          mv[x] = s_ok[g] ? (left ? m : -m) : 0.0;
+          for (int t = 0; t < D; ++t)
+            mm[t][x] = s_ok[g] ? -jump * gg[(left ? 1 : 1 + D) + t] : 0.0;
         }
       }
       __syncthreads();
-      face_scatter<D, N>(T, C, tau, p, mv, mm[0], mm[1], mm[2], sv, sg, tmp);
+      face_scatter<D, N, G>(T, C, tau, p, mv, mm[0], mm[1], mm[2], sv, sg, tmp);
     }
   }
-  for (int e = threadIdx.x; e < ND; e += blockDim.x)
-    P.out[cell * ND + e] = P.b ? P.b[cell * ND + e] - C[e] : C[e];
+  for (int x = threadIdx.x; x < G * ND; x += blockDim.x) {
+    const int64_t cell = cell0 + x / ND;
+    if (cell < ncells) {
+      const int64_t gx = cell * ND + x % ND;
+      P.out[gx] = P.b ? P.b[gx] - C[x] : C[x];
+    }
+  }
 }
 
 // Surrogate cell solves on multilinear levels (fastdiag.py:381-436, 457-496):
@@ -354,13 +383,14 @@ static int launch_dist(const DistArgs& a, const double* u, const double* b, doub
     }
   constexpr int ND = D == 3 ? N * N * N : N * N;
   constexpr int FT = D == 3 ? N * N : N;
-  const size_t smem = sizeof(double) * (7 * (size_t)ND + 20 * (size_t)FT);
+  constexpr int G = dist_cells<D, N>();
+  const size_t smem = sizeof(double) * G * (7 * (size_t)ND + 19 * (size_t)FT);
   auto k = dist_apply_kernel<D, N>;
   if (smem > 48 * 1024)
     DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int64_t ncells = 1;
   for (int t = 0; t < D; ++t) ncells *= a.ncells_dim;
-  k<<<(unsigned)ncells, 128, smem, st>>>(P);
+  k<<<(unsigned)((ncells + G - 1) / G), 128, smem, st>>>(P, ncells);
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }

@@ -159,9 +159,10 @@ def _grad_table(d: int, ref: np.ndarray) -> np.ndarray:
     return out
 
 
-def _adjugate(j: np.ndarray) -> np.ndarray:
+def _adjugate(j):
+    """Adjugate of (..., d, d) (numpy or torch), adj = det J^-1."""
     d = j.shape[-1]
-    adj = np.empty_like(j)
+    adj = j.new_empty(j.shape) if isinstance(j, torch.Tensor) else np.empty_like(j)
     if d == 2:
         adj[..., 0, 0], adj[..., 1, 1] = j[..., 1, 1], j[..., 0, 0]
         adj[..., 0, 1], adj[..., 1, 0] = -j[..., 0, 1], -j[..., 1, 0]
@@ -175,10 +176,10 @@ def _adjugate(j: np.ndarray) -> np.ndarray:
     return adj
 
 
-def _det(j: np.ndarray) -> np.ndarray:
+def _det(j):
     if j.shape[-1] == 2:
         return j[..., 0, 0] * j[..., 1, 1] - j[..., 0, 1] * j[..., 1, 0]
-    return np.linalg.det(j)
+    return torch.linalg.det(j) if isinstance(j, torch.Tensor) else np.linalg.det(j)
 
 
 def _tensor_points(pts: np.ndarray, k: int) -> np.ndarray:
@@ -197,35 +198,40 @@ def _tensor_weights(w: np.ndarray, k: int) -> np.ndarray:
 
 
 class DistortedGeometry:
-    """Host geometry of a multilinear level, packed for the device kernel.
+    """Geometry of a multilinear level, packed for the device kernel and
+    computed with torch on `device` (the GPU by default: a 16.8M-dof level's
+    geometry costs seconds in numpy).
 
     metric:   (B, Q, S)       detJ J^-1 J^-T w (symmetric pairs `_SYM`)
+    detjw:    (B, Q)          detJ w (load vector)
     faces[t]: (F_t, qf, 1+2d) [pen_half, t_plus(d), t_minus(d)] interior
     bnd[t][p]:(F_b, qf, 1+d)  [pen_bnd, t_bnd(d)] boundary side p
     """
 
-    def __init__(self, level: DistortedLevel, basis: Basis1D, gamma_hat: float):
+    def __init__(self, level: DistortedLevel, basis: Basis1D, gamma_hat: float, device=None):
+        if device is None:
+            device = "cuda" if torch.cuda.is_available() else "cpu"
+        dev = torch.device(device)
+        T = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)  # noqa: E731
         d, n, k = level.dim, level.ncells_dim, basis.degree
         pts, w = np.asarray(basis.qpts, float), np.asarray(basis.qwts, float)
-        corners = level.cell_corners()
+        corners = T(level.cell_corners())
         ref = _tensor_points(pts, d)
-        wq = _tensor_weights(w, d)
-        dn = _grad_table(d, ref)
-        jac = np.einsum("fcx,cqt->fqxt", corners, dn)
+        wq = T(_tensor_weights(w, d))
+        jac = torch.einsum("fcx,cqt->fqxt", corners, T(_grad_table(d, ref)))
         det = _det(jac)
-        if np.any(det <= 0.0):
+        if bool(torch.any(det <= 0.0)):
             raise ValueError("nonpositive Jacobian at a quadrature point")
         adj = _adjugate(jac)
         self.detjw = det * wq
         self.ref = ref
-        g = np.einsum("fqxt,fqxs->fqts", adj, adj)
-        self.metric = np.empty(det.shape + (len(_SYM[d]),))
-        for j_, (a, b) in enumerate(_SYM[d]):
-            self.metric[:, :, j_] = g[:, :, a, b] / det * wq
-        cellvol = (det * wq).sum(axis=1)
+        g = torch.einsum("fqxt,fqxs->fqts", adj, adj)
+        self.metric = torch.stack([g[:, :, a, b] / det * wq for a, b in _SYM[d]], dim=-1)
+        del jac, adj, g
+        cellvol = self.detjw.sum(dim=1)
         cgrid = corners.reshape((n,) * d + (2 ** d, d))
         vgrid = cellvol.reshape((n,) * d)
-        wf = _tensor_weights(w, d - 1)
+        wf = T(_tensor_weights(w, d - 1))
         self.faces, self.bnd = [], []
         for tau in range(1, d + 1):
             ax = d - tau
@@ -240,42 +246,42 @@ class DistortedGeometry:
                 return out
 
             def slab(arr, sl_ax):
-                s = [slice(None)] * d
-                s[ax] = sl_ax
-                return arr[tuple(s)]
+                s_ = [slice(None)] * d
+                s_[ax] = sl_ax
+                return arr[tuple(s_)]
 
-            dn_l, dn_r = _grad_table(d, fref(1.0)), _grad_table(d, fref(0.0))
+            dn_l, dn_r = T(_grad_table(d, fref(1.0))), T(_grad_table(d, fref(0.0)))
             cl = slab(cgrid, slice(0, n - 1)).reshape(-1, 2 ** d, d)
             cr = slab(cgrid, slice(1, n)).reshape(-1, 2 ** d, d)
-            vl = slab(vgrid, slice(0, n - 1)).ravel()
-            vr = slab(vgrid, slice(1, n)).ravel()
-            jl = np.einsum("fcx,cqt->fqxt", cl, dn_l)
-            jr = np.einsum("fcx,cqt->fqxt", cr, dn_r)
+            vl = slab(vgrid, slice(0, n - 1)).reshape(-1)
+            vr = slab(vgrid, slice(1, n)).reshape(-1)
+            jl = torch.einsum("fcx,cqt->fqxt", cl, dn_l)
+            jr = torch.einsum("fcx,cqt->fqxt", cr, dn_r)
             adl, adr = _adjugate(jl), _adjugate(jr)
             nvec = adl[:, :, tau - 1, :]
-            nn = np.linalg.norm(nvec, axis=-1)
-            area = (nn * wf).sum(axis=1)
+            nn = torch.linalg.vector_norm(nvec, dim=-1)
+            area = (nn * wf).sum(dim=1)
             ge = gamma_hat * k * (k + 1) * (area / vl + area / vr)
-            pack = np.empty(nn.shape + (1 + 2 * d,))
+            pack = torch.empty(nn.shape + (1 + 2 * d,), dtype=torch.float64, device=dev)
             pack[..., 0] = 0.5 * ge[:, None] * nn * wf
-            pack[..., 1:1 + d] = np.einsum("fqts,fqs->fqt", adl, nvec) / _det(jl)[..., None] \
+            pack[..., 1:1 + d] = torch.einsum("fqts,fqs->fqt", adl, nvec) / _det(jl)[..., None] \
                 * (0.5 * wf)[None, :, None]
-            pack[..., 1 + d:] = np.einsum("fqts,fqs->fqt", adr, nvec) / _det(jr)[..., None] \
+            pack[..., 1 + d:] = torch.einsum("fqts,fqs->fqt", adr, nvec) / _det(jr)[..., None] \
                 * (0.5 * wf)[None, :, None]
             self.faces.append(pack)
             sides = []
             for p, (sl_ax, dnb, sign) in enumerate(((slice(0, 1), dn_r, -1.0),
                                                     (slice(n - 1, n), dn_l, 1.0))):
                 cb = slab(cgrid, sl_ax).reshape(-1, 2 ** d, d)
-                jb = np.einsum("fcx,cqt->fqxt", cb, dnb)
+                jb = torch.einsum("fcx,cqt->fqxt", cb, dnb)
                 adb = _adjugate(jb)
                 nb = sign * adb[:, :, tau - 1, :]
-                nbn = np.linalg.norm(nb, axis=-1)
-                area_b = (nbn * wf).sum(axis=1)
-                ge_b = gamma_hat * k * (k + 1) * (2.0 * area_b / slab(vgrid, sl_ax).ravel())
-                pb = np.empty(nbn.shape + (1 + d,))
+                nbn = torch.linalg.vector_norm(nb, dim=-1)
+                area_b = (nbn * wf).sum(dim=1)
+                ge_b = gamma_hat * k * (k + 1) * (2.0 * area_b / slab(vgrid, sl_ax).reshape(-1))
+                pb = torch.empty(nbn.shape + (1 + d,), dtype=torch.float64, device=dev)
                 pb[..., 0] = ge_b[:, None] * nbn * wf
-                pb[..., 1:] = np.einsum("fqts,fqs->fqt", adb, nb) / _det(jb)[..., None] \
+                pb[..., 1:] = torch.einsum("fqts,fqs->fqt", adb, nb) / _det(jb)[..., None] \
                     * wf[None, :, None]
                 sides.append(pb)
             self.bnd.append(sides)
@@ -303,7 +309,7 @@ class DistortedContext:
             require_cuda()
             dev = torch.device("cuda")
             g = self.geom
-            t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+            t = lambda a: a.to(dev).contiguous()  # noqa: E731
             self._dev = {
                 "metric": t(g.metric),
                 "faces": [t(f) for f in g.faces],
@@ -403,15 +409,33 @@ def surrogate_lengths(corners: np.ndarray) -> np.ndarray:
     return out
 
 
-def _batched_geneig(a: np.ndarray, m: np.ndarray):
-    """Z^T A Z = diag(lam), Z^T M Z = I for stacks (B, n, n) (Cholesky
-    reduction + symmetric eigensolve, host)."""
-    chol = np.linalg.cholesky(m)
-    c = np.linalg.solve(chol, a)
-    c = np.linalg.solve(chol, c.transpose(0, 2, 1))
-    c = 0.5 * (c + c.transpose(0, 2, 1))
-    lam, v = np.linalg.eigh(c)
-    return np.linalg.solve(chol.transpose(0, 2, 1), v), lam
+def _eigh_batched(c):
+    """Batched symmetric eigensolve of small matrices: cuSOLVER in chunks, the
+    host LAPACK for any chunk cuSOLVER's batched path rejects (it fails on
+    large batches of tiny matrices on this stack)."""
+    lams, vs = [], []
+    step = 4096
+    for i in range(0, c.shape[0], step):
+        blk = c[i:i + step].contiguous()
+        try:
+            lam, v = torch.linalg.eigh(blk)
+        except RuntimeError:
+            ln, vn = np.linalg.eigh(blk.cpu().numpy())
+            lam, v = torch.from_numpy(ln).to(c.device), torch.from_numpy(vn).to(c.device)
+        lams.append(lam)
+        vs.append(v)
+    return torch.cat(lams), torch.cat(vs)
+
+
+def _batched_geneig(a, m):
+    """Z^T A Z = diag(lam), Z^T M Z = I for stacks (B, n, n): Cholesky
+    reduction + symmetric eigensolve (torch: batched on the device)."""
+    chol = torch.linalg.cholesky(m)
+    c = torch.linalg.solve_triangular(chol, a, upper=False)
+    c = torch.linalg.solve_triangular(chol, c.transpose(1, 2), upper=False)
+    c = 0.5 * (c + c.transpose(1, 2))
+    lam, v = _eigh_batched(c)
+    return torch.linalg.solve_triangular(chol.transpose(1, 2), v, upper=True), lam
 
 
 class SurrogateCellSolverSet:
@@ -424,22 +448,26 @@ class SurrogateCellSolverSet:
         lvl, b = ctx.level, ctx.basis
         d, n, nn, k = lvl.dim, lvl.ncells_dim, b.n, b.degree
         self.ctx, self.dim, self.n1 = ctx, d, nn
-        hbar = surrogate_lengths(lvl.cell_corners())
+        dev = torch.device("cuda")
+        hbar = torch.as_tensor(surrogate_lengths(lvl.cell_corners()), device=dev)
         B = lvl.ncells
         w = np.asarray(b.qwts, float)
-        mref = (b.values * w) @ b.values.T
-        lref = (b.grads * w) @ b.grads.T
+        T = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)  # noqa: E731
+        mref = T((b.values * w) @ b.values.T)
+        lref = T((b.grads * w) @ b.grads.T)
         bv, bg = b.bv, b.bg
         zs, lams = [], []
+        ids = torch.arange(B, device=dev)
         for t in range(d):
-            pos = (np.arange(B) // n ** t) % n
+            pos = (ids // n ** t) % n
             h = hbar[:, t]
             ge = ctx.gamma_hat * k * (k + 1) * (2.0 / h)
-            eta = (np.where(pos == 0, 1.0, 0.5), np.where(pos == n - 1, 1.0, 0.5))
+            one, half = torch.ones_like(h), torch.full_like(h, 0.5)
+            eta = (torch.where(pos == 0, one, half), torch.where(pos == n - 1, one, half))
             a = lref[None] / h[:, None, None]
             for p in (0, 1):
-                g1 = (-1.0 if p == 0 else 1.0) * np.outer(bv[p], bg[p])
-                a = a + (ge * eta[p])[:, None, None] * np.outer(bv[p], bv[p])[None] \
+                g1 = T((-1.0 if p == 0 else 1.0) * np.outer(bv[p], bg[p]))
+                a = a + (ge * eta[p])[:, None, None] * T(np.outer(bv[p], bv[p]))[None] \
                     - (eta[p] / h)[:, None, None] * (g1 + g1.T)[None]
             z, lam = _batched_geneig(a, h[:, None, None] * mref[None])
             zs.append(z)
@@ -450,11 +478,10 @@ class SurrogateCellSolverSet:
             shape[1 + t] = nn
             arr = lams[t].reshape(shape)
             inv = arr if inv is None else inv + arr
-        if np.any(inv <= 0.0):
+        if bool(torch.any(inv <= 0.0)):
             raise SingularLocalSolverError("nonpositive Kronecker-sum eigenvalue")
-        dev = torch.device("cuda")
-        self._z = torch.from_numpy(np.ascontiguousarray(np.stack(zs))).to(dev)
-        self._inv = torch.from_numpy(np.ascontiguousarray((1.0 / inv).reshape(B, -1))).to(dev)
+        self._z = torch.stack(zs).contiguous()
+        self._inv = (1.0 / inv).reshape(B, -1).contiguous()
         self.ncells = B
 
     def solve_partitioned(self, x, r, parts, omega: float) -> None:
@@ -548,7 +575,8 @@ def compute_rhs(ctx: DistortedContext, f, g) -> np.ndarray:
     grads = torch.from_numpy(np.ascontiguousarray(b.grads)).to(dev)
     corners = lvl.cell_corners()
     coords = np.einsum("fcx,cq->fqx", corners, _corner_values(d, geo.ref))
-    fv = np.asarray(f(coords.reshape(-1, d)), dtype=float).reshape(lvl.ncells, -1) * geo.detjw
+    fv = np.asarray(f(coords.reshape(-1, d)), dtype=float).reshape(lvl.ncells, -1) \
+        * geo.detjw.cpu().numpy()
     w = torch.from_numpy(fv).to(dev).reshape((lvl.ncells,) + (nn,) * d)
     rhs = _contract_quad(w, vals, d).reshape(lvl.ncells, -1)
     cidx = np.indices((n,) * d).reshape(d, -1)[::-1].T                  # (ncells, d), v_1 first
@@ -565,7 +593,7 @@ def compute_rhs(ctx: DistortedContext, f, g) -> np.ndarray:
             fref[:, tau - 1] = float(p)
             fc = np.einsum("fcx,cq->fqx", corners[ids], _corner_values(d, fref))
             gv = np.asarray(g(fc.reshape(-1, d)), dtype=float).reshape(len(ids), -1)
-            pack = geo.bnd[tau - 1][p]                                     # (Fb, qf, 1 + d)
+            pack = geo.bnd[tau - 1][p].cpu().numpy()                       # (Fb, qf, 1 + d)
             mv = torch.from_numpy(gv * pack[..., 0]).to(dev)
             mom = [torch.from_numpy(-gv * pack[..., 1 + t]).to(dev) for t in range(d)]
             k_ = len(trans)

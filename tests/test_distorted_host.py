@@ -26,7 +26,9 @@ def test_geometry_consistency():
     d, n, k = 3, 3, 2
     h = D.distort(mesh.build_hierarchy(d, n, 0), 0.0, 1)
     basis = Basis1D.make(k)
-    geo = D.DistortedGeometry(h.levels[0], basis, 1.0)
+    geo = D.DistortedGeometry(h.levels[0], basis, 1.0, device="cpu")
+    geo.metric, geo.detjw = geo.metric.numpy(), geo.detjw.numpy()
+    geo.faces = [f.numpy() for f in geo.faces]
     hh = 1.0 / n
     w = np.asarray(basis.qwts)
     wq = np.multiply.outer(np.multiply.outer(w, w), w).ravel()
