@@ -326,39 +326,74 @@ __global__ void __launch_bounds__(128) dist_apply_kernel(const __grid_constant__
 
 // Surrogate cell solves on multilinear levels (fastdiag.py:381-436, 457-496):
 // x_c += omega (Z_d x .. x Z_1) diag(1/Lambda_c) (Z_d^T x .. x Z_1^T) r_c with
-// per-cell 1D eigenbases Z_t (global memory, staged per CTA in shared).
+// per-cell 1D eigenbases Z_t (global memory, staged in shared memory); small
+// cells are batched G per 128-thread CTA like the operator kernel.
+template <int D, int N, int G, bool TR>
+__device__ __forceinline__ void contract_cells(double* out, const double* in, int dir,
+                                               const double* Zs, int t) {
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  const int stride = dir == 0 ? 1 : (dir == 1 ? N : N * N);
+  for (int e = threadIdx.x; e < G * ND; e += blockDim.x) {
+    const double* M = Zs + ((e / ND) * D + t) * N * N;
+    const int o = (e / stride) % N;
+    const int base = e - o * stride;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(TR ? M[j * N + o] : M[o * N + j], in[base + j * stride], s);
+    out[e] = s;
+  }
+  __syncthreads();
+}
+
 template <int D, int N>
 __global__ void __launch_bounds__(128)
     dist_cell_fdm_kernel(const double* __restrict__ r, double* __restrict__ x,
                          const double* __restrict__ Z, const double* __restrict__ inv,
-                         const int32_t* __restrict__ list, int64_t ncells, double omega) {
+                         const int32_t* __restrict__ list, int64_t nitems, int64_t ncells,
+                         double omega) {
+  constexpr int G = dist_cells<D, N>();
   constexpr int ND = D == 3 ? N * N * N : N * N;
-  __shared__ double T0[ND], T1[ND], Zs[3][N * N];
-  const int64_t cell = list ? list[blockIdx.x] : blockIdx.x;
-  for (int t = 0; t < D; ++t)
-    for (int e = threadIdx.x; e < N * N; e += blockDim.x)
-      Zs[t][e] = Z[((int64_t)t * ncells + cell) * N * N + e];
-  for (int e = threadIdx.x; e < ND; e += blockDim.x) T0[e] = r[cell * ND + e];
+  __shared__ double T0[G * ND], T1[G * ND], Zs[G * D * N * N];
+  __shared__ int64_t s_cell[G];
+  const int64_t i0 = (int64_t)blockIdx.x * G;
+  if (threadIdx.x < G) {
+    const int64_t it = i0 + threadIdx.x;
+    s_cell[threadIdx.x] = it < nitems ? (list ? (int64_t)list[it] : it) : -1;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * D * N * N; e += blockDim.x) {
+    const int g = e / (D * N * N), q = e - g * D * N * N, t = q / (N * N);
+    const int64_t cell = s_cell[g];
+    Zs[e] = cell >= 0 ? Z[((int64_t)t * ncells + cell) * N * N + q - t * N * N] : 0.0;
+  }
+  for (int e = threadIdx.x; e < G * ND; e += blockDim.x) {
+    const int64_t cell = s_cell[e / ND];
+    T0[e] = cell >= 0 ? r[cell * ND + e % ND] : 0.0;
+  }
   __syncthreads();
   double* a = T0;
   double* b = T1;
   for (int t = 0; t < D; ++t) {  // forward: Z^T along each direction
-    contract<D, N, true, false>(b, a, t, Zs[t]);
+    contract_cells<D, N, G, true>(b, a, t, Zs, t);
     double* s = a; a = b; b = s;
   }
-  for (int e = threadIdx.x; e < ND; e += blockDim.x) {  // 1/Lambda, reversed index
+  for (int e = threadIdx.x; e < G * ND; e += blockDim.x) {  // 1/Lambda, reversed index
+    const int64_t cell = s_cell[e / ND];
+    const int el = e % ND;
     int ri;
-    if (D == 3) ri = (e % N) * N * N + ((e / N) % N) * N + e / (N * N);
-    else ri = (e % N) * N + e / N;
-    a[e] *= inv[cell * ND + ri];
+    if (D == 3) ri = (el % N) * N * N + ((el / N) % N) * N + el / (N * N);
+    else ri = (el % N) * N + el / N;
+    a[e] *= cell >= 0 ? inv[cell * ND + ri] : 0.0;
   }
   __syncthreads();
   for (int t = D - 1; t >= 0; --t) {  // backward: Z along each direction
-    contract<D, N, false, false>(b, a, t, Zs[t]);
+    contract_cells<D, N, G, false>(b, a, t, Zs, t);
     double* s = a; a = b; b = s;
   }
-  for (int e = threadIdx.x; e < ND; e += blockDim.x)
-    x[cell * ND + e] = fma(omega, a[e], x[cell * ND + e]);
+  for (int e = threadIdx.x; e < G * ND; e += blockDim.x) {
+    const int64_t cell = s_cell[e / ND];
+    if (cell >= 0) x[cell * ND + e % ND] = fma(omega, a[e], x[cell * ND + e % ND]);
+  }
 }
 
 template <int D, int N>
@@ -422,12 +457,13 @@ extern "C" int dg_dist_cell_fdm(int dim, int degree, int64_t ncells, const doubl
   const int64_t nb = cells ? n_cells : ncells;
   if (nb == 0) return DG_OK;
   cudaStream_t st = (cudaStream_t)stream;
-#define DG_FCASE(D, NN)                                                                     \
-  if (dim == D && n == NN) {                                                               \
-    dist_cell_fdm_kernel<D, NN><<<(unsigned)nb, 128, 0, st>>>(r, x, z, inv, cells, ncells, \
-                                                               omega);                     \
-    DG_CUDA(cudaGetLastError());                                                           \
-    return DG_OK;                                                                          \
+#define DG_FCASE(D, NN)                                                                 \
+  if (dim == D && n == NN) {                                                           \
+    constexpr int G = dist_cells<D, NN>();                                             \
+    dist_cell_fdm_kernel<D, NN><<<(unsigned)((nb + G - 1) / G), 128, 0, st>>>(          \
+        r, x, z, inv, cells, nb, ncells, omega);                                       \
+    DG_CUDA(cudaGetLastError());                                                       \
+    return DG_OK;                                                                      \
   }
   DG_FCASE(2, 2) DG_FCASE(2, 3) DG_FCASE(2, 4) DG_FCASE(2, 5) DG_FCASE(2, 6) DG_FCASE(2, 7)
   DG_FCASE(2, 8) DG_FCASE(3, 2) DG_FCASE(3, 3) DG_FCASE(3, 4) DG_FCASE(3, 5) DG_FCASE(3, 6)
