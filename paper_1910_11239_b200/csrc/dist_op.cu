@@ -162,7 +162,7 @@ __device__ __forceinline__ void face_scatter(const DistTabs<N>& T, double* acc, 
 template <int D, int N>
 __host__ __device__ constexpr int dist_cells() {
   constexpr int ND = D == 3 ? N * N * N : N * N;
-  return ND >= 64 ? 1 : (128 / ND > 8 ? 8 : 128 / ND);
+  return ND > 64 ? 1 : (128 / ND > 8 ? 8 : 128 / ND);
 }
 
 template <int D, int N>
