@@ -324,6 +324,295 @@ __global__ void __launch_bounds__(128) dist_apply_kernel(const __grid_constant__
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register variant for small cells (n^d <= 16 in 2D, n = 2 in 3D): one thread
+// per cell, the cell's nodes, quadrature values and face fields in registers
+// (every index is a compile-time constant after unrolling), the basis tables
+// in the constant bank (kernel parameters), no shared memory and no barriers.
+// Same arithmetic as dist_apply_kernel, term for term.
+
+template <int K, int N, int DIR, bool TR, bool ACC>
+__device__ __forceinline__ void rcon(double* out, const double* in, const double* M) {
+  constexpr int TOT = K == 3 ? N * N * N : (K == 2 ? N * N : N);
+  constexpr int stride = DIR == 0 ? 1 : (DIR == 1 ? N : N * N);
+#pragma unroll
+  for (int e = 0; e < TOT; ++e) {
+    const int o = (e / stride) % N;
+    const int base = e - o * stride;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(TR ? M[j * N + o] : M[o * N + j], in[base + j * stride], s);
+    out[e] = ACC ? out[e] + s : s;
+  }
+}
+
+template <int CNT>
+__device__ __forceinline__ void rload(double* dst, const double* __restrict__ src) {
+  if constexpr (CNT % 2 == 0) {  // 16-byte aligned: CNT even, base 256-byte aligned
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+    for (int i = 0; i < CNT / 2; ++i) {
+      const double2 v = __ldg(s2 + i);
+      dst[2 * i] = v.x;
+      dst[2 * i + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) dst[i] = __ldg(src + i);
+  }
+}
+
+template <int D, int N, int TAU>
+__device__ __forceinline__ void rtraces(const double* bv, const double* bg, const double* X,
+                                        double* tv, double* tg) {
+  constexpr int FT = D == 3 ? N * N : N;
+#pragma unroll
+  for (int e = 0; e < FT; ++e) {
+    double sv = 0.0, sg = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double v = X[elem<D, N>(TAU, e, i)];
+      sv = fma(bv[i], v, sv);
+      sg = fma(bg[i], v, sg);
+    }
+    tv[e] = sv;
+    tg[e] = sg;
+  }
+}
+
+template <int D, int N, int TAU>
+__device__ __forceinline__ void rface_values(const DistTabs<N>& T, const double* tv,
+                                             const double* tg, double* val,
+                                             double (*Gd)[D == 3 ? N * N : N]) {
+  if constexpr (D == 2) {
+    constexpr int tt = TAU == 1 ? 1 : 0;
+    rcon<1, N, 0, false, false>(val, tv, T.V);
+    rcon<1, N, 0, false, false>(Gd[tt], tv, T.Dg);
+    rcon<1, N, 0, false, false>(Gd[TAU - 1], tg, T.V);
+  } else {
+    constexpr int t1 = TAU == 1 ? 1 : 0, t2 = TAU == 3 ? 1 : 2;
+    double tmp[N * N];
+    rcon<2, N, 0, false, false>(tmp, tv, T.V);
+    rcon<2, N, 1, false, false>(val, tmp, T.V);
+    rcon<2, N, 1, false, false>(Gd[t2], tmp, T.Dg);
+    rcon<2, N, 0, false, false>(tmp, tv, T.Dg);
+    rcon<2, N, 1, false, false>(Gd[t1], tmp, T.V);
+    rcon<2, N, 0, false, false>(tmp, tg, T.V);
+    rcon<2, N, 1, false, false>(Gd[TAU - 1], tmp, T.V);
+  }
+}
+
+template <int D, int N, int TAU, int PS>
+__device__ __forceinline__ void rface_scatter(const DistTabs<N>& T, double* C, const double* mval,
+                                              double (*Mm)[D == 3 ? N * N : N]) {
+  constexpr int FT = D == 3 ? N * N : N;
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  double sv[FT], sg[FT];
+  if constexpr (D == 2) {
+    constexpr int tt = TAU == 1 ? 1 : 0;
+    rcon<1, N, 0, true, false>(sv, mval, T.V);
+    rcon<1, N, 0, true, true>(sv, Mm[tt], T.Dg);
+    rcon<1, N, 0, true, false>(sg, Mm[TAU - 1], T.V);
+  } else {
+    constexpr int t1 = TAU == 1 ? 1 : 0, t2 = TAU == 3 ? 1 : 2;
+    double tmp[FT];
+    rcon<2, N, 1, true, false>(tmp, mval, T.V);
+    rcon<2, N, 1, true, true>(tmp, Mm[t2], T.Dg);
+    rcon<2, N, 0, true, false>(sv, tmp, T.V);
+    rcon<2, N, 1, true, false>(tmp, Mm[t1], T.V);
+    rcon<2, N, 0, true, true>(sv, tmp, T.Dg);
+    rcon<2, N, 1, true, false>(tmp, Mm[TAU - 1], T.V);
+    rcon<2, N, 0, true, false>(sg, tmp, T.V);
+  }
+#pragma unroll
+  for (int x = 0; x < ND; ++x) {
+    int i, e;
+    if constexpr (D == 2) {
+      const int i1 = x % N, i2 = x / N;
+      i = TAU == 1 ? i1 : i2;
+      e = TAU == 1 ? i2 : i1;
+    } else {
+      const int i1 = x % N, i2 = (x / N) % N, i3 = x / (N * N);
+      if (TAU == 1) { i = i1; e = i2 + N * i3; }
+      else if (TAU == 2) { i = i2; e = i1 + N * i3; }
+      else { i = i3; e = i1 + N * i2; }
+    }
+    C[x] += T.bv[PS][i] * sv[e] + T.bg[PS][i] * sg[e];
+  }
+}
+
+// one face of the cell (direction TAU, side PS): own side's moments, scattered into C
+template <int D, int N, int TAU, int PS>
+__device__ __forceinline__ void rface(const DistParams<D, N>& P, const double* U, double* C,
+                                      const int* c) {
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  constexpr int FT = D == 3 ? N * N : N;
+  constexpr int t0 = TAU - 1;
+  const DistTabs<N>& T = P.tab;
+  const int n = P.n;
+  double tv[FT], tg[FT], vo[FT], go[D][FT];
+  rtraces<D, N, TAU>(T.bv[PS], T.bg[PS], U, tv, tg);
+  rface_values<D, N, TAU>(T, tv, tg, vo, go);
+  double mv[FT], mm[D][FT];
+  const bool boundary = PS == 0 ? c[t0] == 0 : c[t0] == n - 1;
+  if (boundary) {
+    int64_t f = 0;
+#pragma unroll
+    for (int t = D - 1; t >= 0; --t)
+      if (t != t0) f = f * n + c[t];
+    const double* gb = P.bnd[2 * t0 + PS] + f * FT * (1 + D);
+#pragma unroll
+    for (int e = 0; e < FT; ++e) {
+      const int gi = D == 3 ? (e % N) * N + e / N : e;
+      const double* gg = gb + gi * (1 + D);
+      double m = vo[e] * __ldg(gg);
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        const double w = __ldg(gg + 1 + t);
+        m -= go[t][e] * w;
+        mm[t][e] = -vo[e] * w;
+      }
+      mv[e] = m;
+    }
+  } else {
+    int64_t nid = 0, f = 0;
+#pragma unroll
+    for (int t = D - 1; t >= 0; --t) {
+      nid = nid * n + c[t] + (t == t0 ? (PS == 1 ? 1 : -1) : 0);
+      f = f * (t == t0 ? n - 1 : n) + c[t] - (t == t0 && PS == 0 ? 1 : 0);
+    }
+    double NB[ND];
+    rload<ND>(NB, P.u + nid * ND);
+    double tvn[FT], tgn[FT], vn[FT], gn[D][FT];
+    rtraces<D, N, TAU>(T.bv[1 - PS], T.bg[1 - PS], NB, tvn, tgn);
+    rface_values<D, N, TAU>(T, tvn, tgn, vn, gn);
+    const double* gf = P.faces[t0] + f * FT * (1 + 2 * D);
+    constexpr bool left = PS == 1;
+#pragma unroll
+    for (int e = 0; e < FT; ++e) {
+      const int gi = D == 3 ? (e % N) * N + e / N : e;
+      const double* gg = gf + gi * (1 + 2 * D);
+      const double vp = left ? vo[e] : vn[e], vmn = left ? vn[e] : vo[e];
+      const double jump = vp - vmn;
+      double m = jump * __ldg(gg);
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        const double gp = left ? go[t][e] : gn[t][e];
+        const double gm = left ? gn[t][e] : go[t][e];
+        m -= gp * __ldg(gg + 1 + t) + gm * __ldg(gg + 1 + D + t);
+      }
+      mv[e] = left ? m : -m;
+#pragma unroll
+      for (int t = 0; t < D; ++t) mm[t][e] = -jump * __ldg(gg + (left ? 1 : 1 + D) + t);
+    }
+  }
+  rface_scatter<D, N, TAU, PS>(T, C, mv, mm);
+}
+
+template <int D, int N>
+__host__ __device__ constexpr bool dist_reg_ok() {
+  return (D == 2 && N <= 5) || (D == 3 && N == 2);
+}
+
+template <int D, int N>
+__global__ void __launch_bounds__(128)
+    dist_apply_reg_kernel(const __grid_constant__ DistParams<D, N> P, int64_t ncells) {
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  constexpr int S = D == 3 ? 6 : 3;
+  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= ncells) return;
+  const DistTabs<N>& T = P.tab;
+  int c[3];
+  {
+    int64_t r = cell;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      c[t] = t < D ? (int)(r % P.n) : 0;
+      r /= P.n;
+    }
+  }
+  double U[ND], C[ND];
+  rload<ND>(U, P.u + cell * ND);
+  {  // volume
+    double g[D][ND];
+    if constexpr (D == 3) {
+      double A[ND], B[ND], X[ND];
+      rcon<3, N, 0, false, false>(A, U, T.V);
+      rcon<3, N, 0, false, false>(B, U, T.Dg);
+      rcon<3, N, 1, false, false>(X, B, T.V);   // x12dv
+      rcon<3, N, 2, false, false>(g[0], X, T.V);
+      rcon<3, N, 1, false, false>(X, A, T.Dg);  // x12vd
+      rcon<3, N, 2, false, false>(g[1], X, T.V);
+      rcon<3, N, 1, false, false>(X, A, T.V);   // x12vv
+      rcon<3, N, 2, false, false>(g[2], X, T.Dg);
+    } else {
+      double A[ND], B[ND];
+      rcon<2, N, 0, false, false>(A, U, T.V);
+      rcon<2, N, 0, false, false>(B, U, T.Dg);
+      rcon<2, N, 1, false, false>(g[0], B, T.V);
+      rcon<2, N, 1, false, false>(g[1], A, T.Dg);
+    }
+    double gm[ND * S];
+    rload<ND * S>(gm, P.metric + cell * ND * S);
+#pragma unroll
+    for (int e = 0; e < ND; ++e) {
+      if constexpr (D == 3) {
+        const int q1 = e % N, q2 = (e / N) % N, q3 = e / (N * N);
+        const double* m = gm + (q1 * N * N + q2 * N + q3) * S;  // reversed
+        const double a1 = g[0][e], a2 = g[1][e], a3 = g[2][e];
+        g[0][e] = m[0] * a1 + m[3] * a2 + m[4] * a3;
+        g[1][e] = m[3] * a1 + m[1] * a2 + m[5] * a3;
+        g[2][e] = m[4] * a1 + m[5] * a2 + m[2] * a3;
+      } else {
+        const int q1 = e % N, q2 = e / N;
+        const double* m = gm + (q1 * N + q2) * S;
+        const double a1 = g[0][e], a2 = g[1][e];
+        g[0][e] = m[0] * a1 + m[2] * a2;
+        g[1][e] = m[2] * a1 + m[1] * a2;
+      }
+    }
+    if constexpr (D == 3) {
+      double A[ND], B[ND], X[ND];
+      rcon<3, N, 2, true, false>(A, g[0], T.V);   // s3_1
+      rcon<3, N, 1, true, false>(B, A, T.V);      // s2_1
+      rcon<3, N, 2, true, false>(A, g[1], T.V);   // s3_2
+      rcon<3, N, 1, true, false>(X, A, T.Dg);
+      rcon<3, N, 2, true, false>(A, g[2], T.Dg);  // s3_3
+      rcon<3, N, 1, true, true>(X, A, T.V);       // s2_23
+      rcon<3, N, 0, true, false>(C, B, T.Dg);
+      rcon<3, N, 0, true, true>(C, X, T.V);
+    } else {
+      double A[ND], B[ND];
+      rcon<2, N, 1, true, false>(A, g[0], T.V);
+      rcon<2, N, 1, true, false>(B, g[1], T.Dg);
+      rcon<2, N, 0, true, false>(C, A, T.Dg);
+      rcon<2, N, 0, true, true>(C, B, T.V);
+    }
+  }
+  rface<D, N, 1, 0>(P, U, C, c);
+  rface<D, N, 1, 1>(P, U, C, c);
+  rface<D, N, 2, 0>(P, U, C, c);
+  rface<D, N, 2, 1>(P, U, C, c);
+  if constexpr (D == 3) {
+    rface<D, N, 3, 0>(P, U, C, c);
+    rface<D, N, 3, 1>(P, U, C, c);
+  }
+  double* o = P.out + cell * ND;
+  if (P.b) {
+    double B[ND];
+    rload<ND>(B, P.b + cell * ND);
+#pragma unroll
+    for (int x = 0; x < ND; ++x) C[x] = B[x] - C[x];
+  }
+  if constexpr (ND % 2 == 0) {
+#pragma unroll
+    for (int x = 0; x < ND; x += 2) reinterpret_cast<double2*>(o)[x / 2] = make_double2(C[x], C[x + 1]);
+  } else {
+#pragma unroll
+    for (int x = 0; x < ND; ++x) o[x] = C[x];
+  }
+}
+
 // Surrogate cell solves on multilinear levels (fastdiag.py:381-436, 457-496):
 // x_c += omega (Z_d x .. x Z_1) diag(1/Lambda_c) (Z_d^T x .. x Z_1^T) r_c with
 // per-cell 1D eigenbases Z_t (global memory, staged in shared memory); small
@@ -418,13 +707,20 @@ static int launch_dist(const DistArgs& a, const double* u, const double* b, doub
     }
   constexpr int ND = D == 3 ? N * N * N : N * N;
   constexpr int FT = D == 3 ? N * N : N;
+  int64_t ncells = 1;
+  for (int t = 0; t < D; ++t) ncells *= a.ncells_dim;
+  if constexpr (dist_reg_ok<D, N>()) {
+    if (env_int("DGB_DIST_REG", 1) != 0) {
+      dist_apply_reg_kernel<D, N><<<(unsigned)((ncells + 127) / 128), 128, 0, st>>>(P, ncells);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
+  }
   constexpr int G = dist_cells<D, N>();
   const size_t smem = sizeof(double) * G * (7 * (size_t)ND + 19 * (size_t)FT);
   auto k = dist_apply_kernel<D, N>;
   if (smem > 48 * 1024)
     DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int64_t ncells = 1;
-  for (int t = 0; t < D; ++t) ncells *= a.ncells_dim;
   k<<<(unsigned)((ncells + G - 1) / G), 128, smem, st>>>(P, ncells);
   DG_CUDA(cudaGetLastError());
   return DG_OK;

@@ -121,3 +121,21 @@ def test_criterion_6_distorted_tables():
                                            smoother="acs", mesh_kind="distorted", omega=0.5,
                                            m_pre=2, m_post=2, max_it=120))[0]
     assert acs2.converged and acs2.nu_frac <= 0.7 * acs1[0].nu_frac
+
+
+@pytest.mark.parametrize("d,coarse,k", [(2, 37, 1), (2, 37, 2), (2, 37, 3), (2, 37, 4),
+                                        (3, 9, 1)])
+def test_register_and_shared_operator_kernels_agree(d, coarse, k, monkeypatch):
+    """The one-cell-per-thread register kernel (small cells) and the shared-
+    memory kernel compute the same operator (ragged last CTA: 37^2, 9^3 cells);
+    both are pinned to the reference by the golden cases above."""
+    h = D.distort(mesh.build_hierarchy(d, coarse, 0), 0.25, 7)
+    ctx = D.DistortedContext(h.levels[0], Basis1D.make(k), 4.0)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    u = torch.rand(ctx.ndofs, dtype=torch.float64, device="cuda", generator=g) - 0.5
+    b = torch.rand(ctx.ndofs, dtype=torch.float64, device="cuda", generator=g) - 0.5
+    monkeypatch.setenv("DGB_DIST_REG", "1")
+    reg = D.residual(ctx, u, b, torch.empty_like(u)).clone()
+    monkeypatch.setenv("DGB_DIST_REG", "0")
+    shm = D.residual(ctx, u, b, torch.empty_like(u))
+    assert rel(reg.cpu(), shm.cpu()) <= RTOL

@@ -31,7 +31,10 @@ def timed(fn, reps=10):
     return e0.elapsed_time(e1) / reps
 
 
-for d, n, k in ((2, 1024, 3), (3, 32, 3), (3, 64, 2)):
+CASES = ((2, 1024, 3), (3, 32, 3), (3, 64, 2))
+if os.environ.get("DIST_CASES"):  # e.g. "2,1024,1;2,1024,2"
+    CASES = tuple(tuple(int(v) for v in c.split(",")) for c in os.environ["DIST_CASES"].split(";"))
+for d, n, k in CASES:
     t0 = time.perf_counter()
     h = D.distort(dg.build_hierarchy(d, n, 0), 0.25, 1234)
     t1 = time.perf_counter()
