@@ -511,11 +511,17 @@ __device__ __forceinline__ void rface(const DistParams<D, N>& P, const double* U
 
 template <int D, int N>
 __host__ __device__ constexpr bool dist_reg_ok() {
-  return (D == 2 && N <= 5) || (D == 3 && N == 2);
+  return (D == 2 && N <= 5) || (D == 3 && N <= 3);
+}
+
+// CTAs per SM the register budget targets (176 -> 168 registers at 2D n = 4: 3 CTAs, not 2)
+template <int D, int N>
+__host__ __device__ constexpr int dist_reg_minb() {
+  return D == 2 ? (N == 2 ? 8 : N == 3 ? 5 : N == 4 ? 3 : 2) : (N == 2 ? 4 : 1);
 }
 
 template <int D, int N>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, dist_reg_minb<D, N>())
     dist_apply_reg_kernel(const __grid_constant__ DistParams<D, N> P, int64_t ncells) {
   constexpr int ND = D == 3 ? N * N * N : N * N;
   constexpr int S = D == 3 ? 6 : 3;
@@ -552,18 +558,24 @@ __global__ void __launch_bounds__(128)
       rcon<2, N, 1, false, false>(g[0], B, T.V);
       rcon<2, N, 1, false, false>(g[1], A, T.Dg);
     }
-    double gm[ND * S];
-    rload<ND * S>(gm, P.metric + cell * ND * S);
+    const double* gmc = P.metric + cell * ND * S;
 #pragma unroll
-    for (int e = 0; e < ND; ++e) {
+    for (int e = 0; e < (D == 3 ? ND : 0); ++e) {
       if constexpr (D == 3) {
         const int q1 = e % N, q2 = (e / N) % N, q3 = e / (N * N);
-        const double* m = gm + (q1 * N * N + q2 * N + q3) * S;  // reversed
+        const double2* m2 = reinterpret_cast<const double2*>(gmc + (q1 * N * N + q2 * N + q3) * S);
+        const double2 m01 = __ldg(m2), m23 = __ldg(m2 + 1), m45 = __ldg(m2 + 2);  // reversed
         const double a1 = g[0][e], a2 = g[1][e], a3 = g[2][e];
-        g[0][e] = m[0] * a1 + m[3] * a2 + m[4] * a3;
-        g[1][e] = m[3] * a1 + m[1] * a2 + m[5] * a3;
-        g[2][e] = m[4] * a1 + m[5] * a2 + m[2] * a3;
-      } else {
+        g[0][e] = m01.x * a1 + m23.y * a2 + m45.x * a3;
+        g[1][e] = m23.y * a1 + m01.y * a2 + m45.y * a3;
+        g[2][e] = m45.x * a1 + m45.y * a2 + m23.x * a3;
+      }
+    }
+    if constexpr (D == 2) {  // whole-cell metric block: 16-byte loads (2D is faster so)
+      double gm[ND * S];
+      rload<ND * S>(gm, gmc);
+#pragma unroll
+      for (int e = 0; e < ND; ++e) {
         const int q1 = e % N, q2 = e / N;
         const double* m = gm + (q1 * N + q2) * S;
         const double a1 = g[0][e], a2 = g[1][e];
@@ -685,6 +697,66 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// register variant (small cells): one thread per cell, r_c, the d eigenbases
+// and the intermediate tensors in registers; no shared memory, no barriers
+template <int D, int N>
+__host__ __device__ constexpr bool dist_fdm_reg_ok() {
+  return (D == 2 && N <= 6) || (D == 3 && N <= 4);
+}
+
+template <int D, int N>
+__global__ void __launch_bounds__(128)
+    dist_cell_fdm_reg_kernel(const double* __restrict__ r, double* __restrict__ x,
+                             const double* __restrict__ Z, const double* __restrict__ inv,
+                             const int32_t* __restrict__ list, int64_t nitems, int64_t ncells,
+                             double omega) {
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  constexpr int NN = N * N;
+  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= nitems) return;
+  const int64_t cell = list ? (int64_t)list[it] : it;
+  double a[ND], b[ND], Z0[NN], Z1[NN], Z2[D == 3 ? NN : 1];
+  rload<NN>(Z0, Z + cell * NN);
+  rload<NN>(Z1, Z + (ncells + cell) * NN);
+  if constexpr (D == 3) rload<NN>(Z2, Z + (2 * ncells + cell) * NN);
+  rload<ND>(a, r + cell * ND);
+  rcon<D, N, 0, true, false>(b, a, Z0);  // forward: Z^T along each direction
+  rcon<D, N, 1, true, false>(a, b, Z1);
+  double* f = a;
+  if constexpr (D == 3) {
+    rcon<D, N, 2, true, false>(b, a, Z2);
+    f = b;
+  }
+  double lam[ND];
+  rload<ND>(lam, inv + cell * ND);
+#pragma unroll
+  for (int el = 0; el < ND; ++el) {  // 1/Lambda, reversed index
+    const int ri = D == 3 ? (el % N) * N * N + ((el / N) % N) * N + el / (N * N)
+                          : (el % N) * N + el / N;
+    f[el] *= lam[ri];
+  }
+  if constexpr (D == 3) {  // backward: Z along each direction
+    rcon<D, N, 2, false, false>(a, b, Z2);
+    rcon<D, N, 1, false, false>(b, a, Z1);
+    rcon<D, N, 0, false, false>(a, b, Z0);
+  } else {
+    rcon<D, N, 1, false, false>(b, a, Z1);
+    rcon<D, N, 0, false, false>(a, b, Z0);
+  }
+  double xv[ND];
+  rload<ND>(xv, x + cell * ND);
+  double* o = x + cell * ND;
+  if constexpr (ND % 2 == 0) {
+#pragma unroll
+    for (int e = 0; e < ND; e += 2)
+      reinterpret_cast<double2*>(o)[e / 2] =
+          make_double2(fma(omega, a[e], xv[e]), fma(omega, a[e + 1], xv[e + 1]));
+  } else {
+#pragma unroll
+    for (int e = 0; e < ND; ++e) o[e] = fma(omega, a[e], xv[e]);
+  }
+}
+
 template <int D, int N>
 static int launch_dist(const DistArgs& a, const double* u, const double* b, double* out,
                        cudaStream_t st) {
@@ -726,6 +798,25 @@ static int launch_dist(const DistArgs& a, const double* u, const double* b, doub
   return DG_OK;
 }
 
+template <int D, int N>
+static int launch_cell_fdm(const double* r, double* x, const double* z, const double* inv,
+                           const int32_t* cells, int64_t nb, int64_t ncells, double omega,
+                           cudaStream_t st) {
+  if constexpr (dist_fdm_reg_ok<D, N>()) {
+    if (env_int("DGB_DIST_REG", 1) != 0) {
+      dist_cell_fdm_reg_kernel<D, N><<<(unsigned)((nb + 127) / 128), 128, 0, st>>>(
+          r, x, z, inv, cells, nb, ncells, omega);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
+  }
+  constexpr int G = dist_cells<D, N>();
+  dist_cell_fdm_kernel<D, N><<<(unsigned)((nb + G - 1) / G), 128, 0, st>>>(r, x, z, inv, cells,
+                                                                           nb, ncells, omega);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
 }  // namespace dgb
 
 extern "C" int dg_dist_apply(const dg_dist_args_t* args, const double* u, const double* b,
@@ -753,14 +844,8 @@ extern "C" int dg_dist_cell_fdm(int dim, int degree, int64_t ncells, const doubl
   const int64_t nb = cells ? n_cells : ncells;
   if (nb == 0) return DG_OK;
   cudaStream_t st = (cudaStream_t)stream;
-#define DG_FCASE(D, NN)                                                                 \
-  if (dim == D && n == NN) {                                                           \
-    constexpr int G = dist_cells<D, NN>();                                             \
-    dist_cell_fdm_kernel<D, NN><<<(unsigned)((nb + G - 1) / G), 128, 0, st>>>(          \
-        r, x, z, inv, cells, nb, ncells, omega);                                       \
-    DG_CUDA(cudaGetLastError());                                                       \
-    return DG_OK;                                                                      \
-  }
+#define DG_FCASE(D, NN) \
+  if (dim == D && n == NN) return launch_cell_fdm<D, NN>(r, x, z, inv, cells, nb, ncells, omega, st);
   DG_FCASE(2, 2) DG_FCASE(2, 3) DG_FCASE(2, 4) DG_FCASE(2, 5) DG_FCASE(2, 6) DG_FCASE(2, 7)
   DG_FCASE(2, 8) DG_FCASE(3, 2) DG_FCASE(3, 3) DG_FCASE(3, 4) DG_FCASE(3, 5) DG_FCASE(3, 6)
 #undef DG_FCASE

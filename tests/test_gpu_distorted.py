@@ -124,7 +124,7 @@ def test_criterion_6_distorted_tables():
 
 
 @pytest.mark.parametrize("d,coarse,k", [(2, 37, 1), (2, 37, 2), (2, 37, 3), (2, 37, 4),
-                                        (3, 9, 1)])
+                                        (3, 9, 1), (3, 9, 2)])
 def test_register_and_shared_operator_kernels_agree(d, coarse, k, monkeypatch):
     """The one-cell-per-thread register kernel (small cells) and the shared-
     memory kernel compute the same operator (ragged last CTA: 37^2, 9^3 cells);
@@ -139,3 +139,25 @@ def test_register_and_shared_operator_kernels_agree(d, coarse, k, monkeypatch):
     monkeypatch.setenv("DGB_DIST_REG", "0")
     shm = D.residual(ctx, u, b, torch.empty_like(u))
     assert rel(reg.cpu(), shm.cpu()) <= RTOL
+
+
+@pytest.mark.parametrize("d,coarse,k", [(2, 37, 1), (2, 37, 3), (2, 37, 5), (3, 9, 1),
+                                        (3, 9, 2), (3, 9, 3)])
+def test_register_and_shared_cell_solve_kernels_agree(d, coarse, k, monkeypatch):
+    """Surrogate cell solves: register kernel vs shared-memory kernel, all
+    cells (ACS) and red-black cell lists (MCS)."""
+    from paper_1910_11239_b200.smoothers import SmootherConfig
+    h = D.distort(mesh.build_hierarchy(d, coarse, 0), 0.25, 7)
+    ctx = D.DistortedContext(h.levels[0], Basis1D.make(k), 4.0)
+    n = ctx.ndofs
+    b = np.random.default_rng(1).uniform(-1.0, 1.0, n)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("DGB_DIST_REG", flag)
+        for kind, om in (("acs", 0.5), ("mcs", 0.75)):
+            sm = D.DistortedSmoother(ctx, SmootherConfig(kind=kind, omega=om))
+            x = np.random.default_rng(2).uniform(-1.0, 1.0, n)
+            sm.smooth(x, b)
+            out[flag, kind] = x
+    for kind in ("acs", "mcs"):
+        assert rel(out["1", kind], out["0", kind]) <= RTOL
