@@ -2,7 +2,9 @@
 // row 3 (reference: dgop._volume_apply / _faces_apply non-Cartesian
 // branches, dgop.py:432-481, 583-759; geometry dgop.py:277-374).
 //
-// One CTA per cell, all tensors of the cell in shared memory:
+// Small cells (2D k <= 4, 3D k <= 2) run dist_apply_reg_kernel: one thread per
+// cell with everything in registers (below).  Larger cells run
+// dist_apply_kernel: 1-8 cells per CTA, all tensors of the cells in shared memory:
 //  - volume: the d reference gradients at the n^d Gauss points by
 //    sum-factorised contractions (values / derivative tables per direction,
 //    shared prefixes), the symmetric metric detJ J^-1 J^-T w per point
