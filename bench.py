@@ -347,6 +347,35 @@ def run_ours(args, cfg):
                "ms_per_step": e_ms,
                "api": "LevelSmoother.smooth(pinned host tensors): H2D x,b / D2H x inside the call",
                "pipelined": bool(sm._pipelinable(xh, bh))}
+        # the step's PCIe bound: the same copies alone (x, b in on one stream,
+        # x out on another, concurrently), no kernels
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        xd = torch.empty(n_local, dtype=torch.float64, device="cuda")
+        bd = torch.empty_like(xd)
+
+        def copies():
+            s_in.wait_stream(stream)
+            s_out.wait_stream(stream)
+            with torch.cuda.stream(s_in):
+                xd.copy_(xh, non_blocking=True)
+                bd.copy_(bh, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                xh.copy_(sm._r, non_blocking=True)
+            stream.wait_stream(s_in)
+            stream.wait_stream(s_out)
+        xsave = xh.clone()
+        copies()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(3):
+            copies()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        xh.copy_(xsave)
+        c_ms = e0.elapsed_time(e1) / 3
+        del xd, bd, xsave
+        e2e["copy_bound_ms"] = c_ms
+        e2e["frac_of_copy_bound"] = c_ms / e_ms
     else:
         e2e = step_obj.e2e(x_h, b_h, reps=max(3, min(args.steps, 10)))
         e2e["value"] = e2e.pop("dofs_local") * ws / (e2e["ms_per_step"] * 1e-3)

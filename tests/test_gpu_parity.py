@@ -410,6 +410,31 @@ def test_host_pipelined_step_matches_device_step(kind, omega, k):
     assert rel(xn, OracleLevel((nc,) * 3, k).smooth(kind, omega, x0, b)) <= RTOL
 
 
+@pytest.mark.parametrize("kind,omega", [("acs", 0.7), ("avs", 0.25)])
+@pytest.mark.parametrize("head,tail,layers", [(4, 4, 4), (2, 6, 6), (0, 8, 2)])
+def test_host_pipelined_uneven_chunks(kind, omega, head, tail, layers, monkeypatch):
+    """2-layer head / tail chunks around the uniform ones (DGB_PIPE_HEAD /
+    DGB_PIPE_TAIL / DGB_PIPE_LAYERS): same result as the device step."""
+    monkeypatch.setenv("DGB_PIPE_HEAD", str(head))
+    monkeypatch.setenv("DGB_PIPE_TAIL", str(tail))
+    monkeypatch.setenv("DGB_PIPE_LAYERS", str(layers))
+    nc = 24
+    ctx, _, sm = _setup(3, nc, 2, kind, omega)
+    bounds = sm._pipe_bounds(nc)
+    assert bounds[0] == 0 and bounds[-1] == nc and all(b > a for a, b in zip(bounds, bounds[1:]))
+    x0, b = inputs(ctx.ndofs, 15)
+    assert sm._pipelinable(x0, b)
+    xd = torch.from_numpy(x0).cuda()
+    sm.smooth(xd, torch.from_numpy(b).cuda())
+    want = xd.cpu().numpy()
+    xn = x0.copy()
+    sm.smooth(xn, b)
+    if kind == "acs":
+        assert np.array_equal(xn, want)
+    else:
+        assert rel(xn - x0, want - x0) <= 1e-14
+
+
 @pytest.mark.parametrize("k", [3, 5])
 def test_mvs_block_list_residual_bitwise(k, monkeypatch):
     """The MVS restricted residual on vertex-patch cell lists runs in 2x2x2
