@@ -45,3 +45,34 @@ def test_surrogate_lengths_of_boxes():
     for c in range(8):
         corners[0, c] = [(c & 1) * 0.5, ((c >> 1) & 1) * 0.25, ((c >> 2) & 1) * 2.0]
     assert np.allclose(D.surrogate_lengths(corners), [[0.5, 0.25, 2.0]])
+
+
+def test_patch_solvers_reject_distorted_levels():
+    """`test_fastdiag.py:233-240`: vertex-patch solver sets need Cartesian
+    levels (ValueError)."""
+    from paper_1910_11239_b200.fastdiag import PatchSolverSet
+    h = D.distort(mesh.build_hierarchy(2, 2, 1), 0.2, 1)
+    with pytest.raises(ValueError):
+        PatchSolverSet(h.levels[1], Basis1D.make(2), 4.0)
+
+
+def test_surrogate_degenerate_edge_raises():
+    """`test_mesh.py:206-209`: a zero-length cell edge is rejected."""
+    corners = np.array([[0.0, 0.0], [0.0, 0.0], [0.0, 1.0], [0.0, 1.0]])
+    with pytest.raises(ValueError):
+        D.surrogate_lengths(corners)
+
+
+def test_distortion_factor_range():
+    """`mesh.py:227-284`: the perturbation factor must lie in [0, 0.5)."""
+    for bad in (-0.1, 0.5):
+        with pytest.raises(ValueError):
+            D.distort(mesh.build_hierarchy(2, 2, 0), bad, 1)
+
+
+def test_dense_assembly_size_guard():
+    """`test_dgop.py:301-304`: dense assembly refuses large levels."""
+    from paper_1910_11239_b200 import dgop
+    ctx = dgop.make_context(mesh.build_hierarchy(2, 2, 5).levels[5], Basis1D.make(3))
+    with pytest.raises(ValueError):
+        dgop.assemble_dense(ctx)
