@@ -211,7 +211,11 @@ def run_ours(args, cfg):
     slab = ws > 1 or args.slab
     if slab:
         # keep stdout to the one JSON line (NCCL prints its version otherwise)
-        os.environ.setdefault("NCCL_DEBUG", "WARN")
+        # (the image's Python starts with NCCL_DEBUG=VERSION, which prints the
+        # version line on stdout: lower it, and send any NCCL log to stderr)
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if not dist.is_initialized():
             if ws == 1:
                 os.environ.setdefault("MASTER_ADDR", "127.0.0.1")

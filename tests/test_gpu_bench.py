@@ -48,3 +48,19 @@ def test_reference_arm_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_torchrun_slab_line_is_the_only_stdout():
+    """The driver's N > 1 launch (torchrun, NCCL slabs) at N = 1: rank 0's
+    stdout is exactly the one JSON line (no NCCL version banner)."""
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "1", "--master-addr", "127.0.0.1",
+                          "--master-port", "29517", os.path.join(ROOT, "bench.py"),
+                          "--gpus", "1", "--slab", "--steps", "3",
+                          "--warmup", "3", "--no-cpu"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["e2e"]["value"] > 0
