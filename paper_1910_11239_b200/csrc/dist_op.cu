@@ -703,7 +703,7 @@ __global__ void __launch_bounds__(128)
 // and the intermediate tensors in registers; no shared memory, no barriers
 template <int D, int N>
 __host__ __device__ constexpr bool dist_fdm_reg_ok() {
-  return (D == 2 && N <= 6) || (D == 3 && N <= 4);
+  return (D == 2 && N <= 7) || (D == 3 && N <= 4);
 }
 
 template <int D, int N>

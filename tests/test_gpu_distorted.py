@@ -141,7 +141,7 @@ def test_register_and_shared_operator_kernels_agree(d, coarse, k, monkeypatch):
     assert rel(reg.cpu(), shm.cpu()) <= RTOL
 
 
-@pytest.mark.parametrize("d,coarse,k", [(2, 37, 1), (2, 37, 3), (2, 37, 5), (3, 9, 1),
+@pytest.mark.parametrize("d,coarse,k", [(2, 37, 1), (2, 37, 3), (2, 37, 5), (2, 19, 6), (3, 9, 1),
                                         (3, 9, 2), (3, 9, 3)])
 def test_register_and_shared_cell_solve_kernels_agree(d, coarse, k, monkeypatch):
     """Surrogate cell solves: register kernel vs shared-memory kernel, all
