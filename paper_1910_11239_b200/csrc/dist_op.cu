@@ -2,9 +2,9 @@
 // row 3 (reference: dgop._volume_apply / _faces_apply non-Cartesian
 // branches, dgop.py:432-481, 583-759; geometry dgop.py:277-374).
 //
-// Small cells (2D k <= 4, 3D k <= 2) run dist_apply_reg_kernel: one thread per
-// cell with everything in registers (below).  Larger cells run
-// dist_apply_kernel: 1-8 cells per CTA, all tensors of the cells in shared memory:
+// 2D (all degrees) and 3D k <= 4 run dist_apply_reg_kernel: one thread per
+// cell with everything in registers (below).  3D k = 5 runs dist_apply_kernel:
+// 1-8 cells per CTA, all tensors of the cells in shared memory:
 //  - volume: the d reference gradients at the n^d Gauss points by
 //    sum-factorised contractions (values / derivative tables per direction,
 //    shared prefixes), the symmetric metric detJ J^-1 J^-T w per point
@@ -511,9 +511,11 @@ __device__ __forceinline__ void rface(const DistParams<D, N>& P, const double* U
   rface_scatter<D, N, TAU, PS>(T, C, mv, mm);
 }
 
+// the register kernel wins even where it spills (2D n = 6..8, 3D n = 4, 5:
+// local-memory spills stay in L1); only at 3D n = 6 is the shared kernel faster
 template <int D, int N>
 __host__ __device__ constexpr bool dist_reg_ok() {
-  return (D == 2 && N <= 5) || (D == 3 && N <= 3);
+  return (D == 2 && N <= 8) || (D == 3 && N <= 5);
 }
 
 // CTAs per SM the register budget targets (176 -> 168 registers at 2D n = 4: 3 CTAs, not 2)

@@ -124,7 +124,8 @@ def test_criterion_6_distorted_tables():
 
 
 @pytest.mark.parametrize("d,coarse,k", [(2, 37, 1), (2, 37, 2), (2, 37, 3), (2, 37, 4),
-                                        (3, 9, 1), (3, 9, 2)])
+                                        (2, 19, 5), (2, 19, 6), (2, 19, 7), (3, 9, 1),
+                                        (3, 9, 2), (3, 7, 3), (3, 5, 4), (3, 5, 5)])
 def test_register_and_shared_operator_kernels_agree(d, coarse, k, monkeypatch):
     """The one-cell-per-thread register kernel (small cells) and the shared-
     memory kernel compute the same operator (ragged last CTA: 37^2, 9^3 cells);
