@@ -312,7 +312,9 @@ def run_ours(args, cfg):
         solve_ms, res_ms = kt["solve_ms"], kt["residual_ms"]
         dom_ms, dom_f = (solve_ms, f_solve) if solve_ms >= res_ms else (res_ms, f_res)
         if solve_ms < res_ms:
-            dom = "res2_kernel (residual)"
+            n1 = k + 1  # launch_res.cu: res3 for 3D n = 7..9 and n >= 13 by default
+            res3 = d == 3 and os.environ.get("DGB_RES3", "1") != "0" and 7 <= n1 and (n1 <= 9 or n1 >= 13)
+            dom = f"res3_kernel<{n1}> (residual)" if res3 else f"res2_kernel<{d},{n1}> (residual)"
     achieved = dom_f / (dom_ms * 1e-3) / 1e12
     # the kernels split interior-digit contractions even/odd (half the FMAs):
     # also report the fraction against the flops actually executed
@@ -406,7 +408,9 @@ def run_ours(args, cfg):
                        else "inputs smaller than L2"},
             "roofline": {"bound": "tensor", "pipe": "fp64 (DFMA/DMMA)", "kernel": dom,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak,
+                         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                         "traffic_detail": traffic,
                          "work_model": "SURVEY 8(d) dense contractions (FMA = 2)",
                          "achieved_executed": dom_fx / (dom_ms * 1e-3) / 1e12,
                          "frac_executed": dom_fx / (dom_ms * 1e-3) / 1e12 / peak,
