@@ -162,6 +162,26 @@ def test_avs_full_cfg5_linear_in_b():
     assert float((d2 - 2 * d1).norm()) <= 1e-12 * float(d2.norm())
 
 
+def test_cfg5_host_pipelined_step_matches_device_step():
+    """cfg 5 at full size through the e2e path: pinned host tensors take the
+    pipelined step (16 z-chunks + 2-layer tail chunks, H2D / residual / range
+    solves / D2H overlapped) and give the device-resident step's update to
+    rounding (both accumulate the patch updates with bulk fp64 reduce-adds)."""
+    ctx, _, sm = _setup(3, 64, 5, "avs", 0.25)
+    x0, b = inputs(ctx.ndofs, 0)
+    xh = torch.from_numpy(x0.copy()).pin_memory()
+    bh = torch.from_numpy(b).pin_memory()
+    assert sm._pipelinable(xh, bh)
+    bounds = sm._pipe_bounds(64)
+    assert bounds[-1] == 64 and bounds[-2] == 62  # the tail chunks are in use
+    sm.smooth(xh, bh)
+    xd = torch.from_numpy(x0).cuda()
+    sm.smooth(xd, bh.cuda())
+    want = xd.cpu() - torch.from_numpy(x0)
+    got = xh - torch.from_numpy(x0)
+    assert float((got - want).norm()) <= 1e-13 * float(want.norm())
+
+
 def test_graph_and_direct_launch_agree_bitwise():
     ctx, _, sm = _setup(3, 6, 3, "mvs", 1.0)
     x0, b = inputs(ctx.ndofs)
