@@ -327,11 +327,13 @@ __global__ void __launch_bounds__(128) dist_apply_kernel(const __grid_constant__
 }
 
 // ---------------------------------------------------------------------------
-// Register variant for small cells (n^d <= 16 in 2D, n = 2 in 3D): one thread
-// per cell, the cell's nodes, quadrature values and face fields in registers
-// (every index is a compile-time constant after unrolling), the basis tables
-// in the constant bank (kernel parameters), no shared memory and no barriers.
-// Same arithmetic as dist_apply_kernel, term for term.
+// Register variant (2D all degrees, 3D k <= 4; dist_reg_ok): one thread per
+// cell, the cell's nodes, quadrature values and face fields in registers
+// (every index is a compile-time constant after unrolling; from 2D n = 6 /
+// 3D n = 4 the surplus spills to L1-resident local memory and still beats
+// the shared kernel), the basis tables in the constant bank (kernel
+// parameters), no shared memory and no barriers.  Same arithmetic as
+// dist_apply_kernel, term for term.
 
 template <int K, int N, int DIR, bool TR, bool ACC>
 __device__ __forceinline__ void rcon(double* out, const double* in, const double* M) {
@@ -701,7 +703,7 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// register variant (small cells): one thread per cell, r_c, the d eigenbases
+// register variant (2D k <= 6, 3D k <= 3): one thread per cell, r_c, the d eigenbases
 // and the intermediate tensors in registers; no shared memory, no barriers
 template <int D, int N>
 __host__ __device__ constexpr bool dist_fdm_reg_ok() {
