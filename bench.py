@@ -16,9 +16,10 @@ Inputs: b, x0 ~ U[-1,1] from seeds 0/1 (synthetic); every vector
 `value` is device-timed (CUDA events, max over ranks) with inputs resident in
 HBM; `e2e` times the public API (`LevelSmoother.smooth`) with the host->device
 copy of x and b from pinned memory and the device->host copy of x inside the
-timed region.  `--impl reference` times the CPU oracle port of the reference
-algorithm (oracle/sipg_oracle.py; the reference itself is Python and cannot
-travel to the GPU box) on a bounded sample of the same workload.
+timed region.  `--impl reference` times the reference itself (the unmodified
+`dgmg` package, pip-installed by `build()` into the git-ignored `baseline/_ref`,
+which travels to the GPU box) on the host cores, `LevelSmoother.smooth` on the
+same level; `cpu_baseline` in our line is the same measurement (one step).
 """
 
 from __future__ import annotations
@@ -124,77 +125,162 @@ def _dist_env():
     return ws, rank, local
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return None
+
+
+def _load_reference():
+    """The unmodified reference package `dgmg`, installed by `build()` into the
+    git-ignored `baseline/_ref` (pip --target of /root/reference/pkg; it
+    travels to the GPU box with the snapshot).  None when absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "dgmg")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import dgmg  # noqa: F401
+    from dgmg import dgop, mesh, polybasis, smoothers
+    if not os.path.abspath(dgop.__file__).startswith(os.path.abspath(REF_DIR)):
+        raise RuntimeError(f"dgmg imported from {dgop.__file__}, not {REF_DIR}")
+    return mesh, polybasis, dgop, smoothers
+
+
+class RefStep:
+    """One smoothing step of the reference itself on `dims` cells:
+    `mesh.build_hierarchy(d, n_c, 0)`, `make_context`, `make_level_smoother(ctx, basis, SmootherConfig(kind,
+    omega))`, then `LevelSmoother.smooth(x, b)` on the seeded inputs
+    (reference `smoothers.py:131-197`, `dgop.py:399-411`)."""
+
+    def __init__(self, cfg, dims):
+        mods = _load_reference()
+        if mods is None:
+            raise FileNotFoundError("baseline/_ref/dgmg not installed")
+        mesh, polybasis, dgop, smoothers = mods
+        d, k = cfg["d"], cfg["k"]
+        t0 = time.perf_counter()
+        if len(set(dims)) != 1:
+            raise ValueError("the reference builds cubes only (mesh.py:142-157)")
+        lvl = mesh.build_hierarchy(d, dims[0], 0).levels[0]
+        basis = polybasis.Basis1D.make(k)
+        self.ctx = dgop.make_context(lvl, basis, 1.0)
+        self.sm = smoothers.make_level_smoother(
+            self.ctx, basis, smoothers.SmootherConfig(kind=cfg["kind"], omega=cfg["omega"]))
+        self.setup_s = time.perf_counter() - t0
+        self.ndofs = self.ctx.ndofs
+        self.b = np.random.default_rng(0).uniform(-1.0, 1.0, self.ndofs)
+        self.x0 = np.random.default_rng(1).uniform(-1.0, 1.0, self.ndofs)
+
+    def __call__(self):
+        x = self.x0.copy()
+        t0 = time.perf_counter()
+        self.sm.smooth(x, self.b)
+        return time.perf_counter() - t0
+
+
+class PortStep:
+    """Fallback when baseline/_ref is missing: the oracle port (numpy)."""
+
+    def __init__(self, cfg, dims):
+        from oracle.sipg_oracle import OracleLevel, seeded_inputs
+        t0 = time.perf_counter()
+        self.lvl = OracleLevel(tuple(dims), cfg["k"], h=1.0 / dims[0])
+        self.setup_s = time.perf_counter() - t0
+        self.ndofs = self.lvl.ndofs
+        self.x0, self.b = seeded_inputs(self.ndofs, 0)
+        self.kind, self.omega = cfg["kind"], cfg["omega"]
+
+    def __call__(self):
+        t0 = time.perf_counter()
+        self.lvl.smooth(self.kind, self.omega, self.x0, self.b)
+        return time.perf_counter() - t0
+
+
+def _cpu_step(cfg, dims):
+    try:
+        return RefStep(cfg, dims), "reference"
+    except (FileNotFoundError, ImportError):
+        return PortStep(cfg, dims), "port"
+
+
+def config_dict(cfg, dims, ws, n_global, slab):
+    """The `config` object both arms print (identical, so the driver's
+    same-config check can hold)."""
+    n_local = n_global // ws
+    return {"workload": cfg["name"], "dims": list(dims), "k": cfg["k"], "kind": cfg["kind"],
+            "omega": cfg["omega"], "global_dofs": n_global,
+            "parallelism": f"slab{ws}" if slab else "single",
+            "l2": "inputs larger than L2 (no flush)" if n_local * 8 > 126e6
+            else "inputs smaller than L2"}
+
+
+def _bench_dims(cfg, ws, slab):
+    d, nc = cfg["d"], cfg["nc"]
+    return (nc,) * d if not slab else (nc, nc, nc * ws)
+
+
 def run_reference(args, cfg):
-    """CPU oracle port of the reference path on a bounded sample (rank 0)."""
+    """The reference's own CPU implementation (`dgmg`, unmodified, from
+    baseline/_ref) timed on the box's host cores: W untimed + K timed
+    `LevelSmoother.smooth` steps on the same level as our arm (rank 0 only;
+    at N > 1 the per-GPU 64^3 share, since the CPU rate is size-independent
+    and the 64x64x64N box does not fit a CPU process at N = 8)."""
     ws, rank, _ = _dist_env()
     if rank != 0:
         return
-    from oracle.sipg_oracle import OracleLevel, seeded_inputs
+    slab = ws > 1 or args.slab
+    dims = _bench_dims(cfg, ws, slab)
+    run_dims = dims if not slab else (cfg["nc"],) * 3
+    step, kind = _cpu_step(cfg, run_dims)
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    t = float(np.mean(times))
+    value = step.ndofs / t
     cores = len(os.sched_getaffinity(0))
-    d, nc, k = cfg["d"], cfg["nc"], cfg["k"]
-    # bounded sample: a slab of the same box (all of it for small configs)
-    if args.config == 5:
-        dims = (nc, nc, 4)
-        sample = f"64x64x4-cell slab of the 64^3 Q5 box ({nc * nc * 4 * 216} DoFs), one AVS step"
-    elif args.config == 3:
-        dims = (nc, nc, 4)
-        sample = "32x32x4-cell slab of the 32^3 Q7 box, one MVS sweep (16 colours)"
-    else:
-        dims = (nc,) * d
-        sample = "full level, one step"
-    lvl = OracleLevel(dims, k, h=1.0 / nc)
-    x0, b = seeded_inputs(lvl.ndofs, 0)
-    for _ in range(max(1, min(args.warmup, 1))):
-        lvl.smooth(cfg["kind"], cfg["omega"], x0, b)
-    t0 = time.perf_counter()
-    lvl.smooth(cfg["kind"], cfg["omega"], x0, b)
-    t_one = time.perf_counter() - t0
-    # bounded: at most ~150 s of timed CPU work whatever --steps says
-    n_run = max(1, min(args.steps, int(150.0 / max(t_one, 1e-3))))
-    times = []
-    for _ in range(n_run):
-        t0 = time.perf_counter()
-        lvl.smooth(cfg["kind"], cfg["omega"], x0, b)
-        times.append(time.perf_counter() - t0)
-    t = float(np.median(times))
-    value = lvl.ndofs / t
+    what = "dgmg (unmodified reference, baseline/_ref)" if kind == "reference" else \
+        "oracle port (baseline/_ref missing)"
+    sample = (f"{what}: LevelSmoother.smooth on {'x'.join(map(str, run_dims))} cells "
+              f"({step.ndofs} DoFs), one step per timed step; setup {step.setup_s:.1f} s excluded")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DoF/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded uniform[-1,1])",
-        "config": {"workload": cfg["name"], "sample": sample, "k": k, "kind": cfg["kind"],
-                   "omega": cfg["omega"], "steps_run": n_run},
-        "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "data": "synthetic (seeded uniform[-1,1] b, x0)",
+        "config": config_dict(cfg, dims, ws, step.ndofs * (ws if slab else 1), slab),
+        "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": cores, "kind": kind,
+                         "sample": sample, "cpu_model": _cpu_model(),
+                         "blas_threads": cores, "min_ms": min(times) * 1e3,
+                         "max_ms": max(times) * 1e3},
         "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(cfg, config_id, budget_s=20.0):
-    """Oracle step on a bounded sample (rank 0, N=1), all host threads."""
-    from oracle.sipg_oracle import OracleLevel, seeded_inputs
-    d, nc, k = cfg["d"], cfg["nc"], cfg["k"]
-    if config_id == 5:
-        dims, sample = (nc, nc, 8), "one AVS step on a 64x64x8-cell slab of the Q5 box"
-    elif config_id == 3:
-        dims, sample = (nc, nc, 4), "one MVS sweep on a 32x32x4-cell slab of the Q7 box"
-    else:
-        dims, sample = (nc,) * d, "one step on the full level"
-    lvl = OracleLevel(dims, k, h=1.0 / nc)
-    x0, b = seeded_inputs(lvl.ndofs, 0)
+def cpu_baseline_sample(cfg, dims, budget_s=30.0):
+    """The reference's step on the same level (rank 0, N = 1), all host
+    threads: one step for the large configs (~20 s), up to 5 for small ones."""
+    step, kind = _cpu_step(cfg, dims)
     times = []
     t_all = time.perf_counter()
     while True:
-        t0 = time.perf_counter()
-        lvl.smooth(cfg["kind"], cfg["omega"], x0, b)
-        times.append(time.perf_counter() - t0)
+        times.append(step())
         if time.perf_counter() - t_all > budget_s or len(times) >= 5:
             break
     t = float(min(times))
-    return {"value": lvl.ndofs / t, "unit": "DoF/s", "cores": len(os.sched_getaffinity(0)),
-            "kind": "port", "sample": f"{sample}, best of {len(times)}"}
+    what = "dgmg (unmodified reference)" if kind == "reference" else "oracle port"
+    return {"value": step.ndofs / t, "unit": "DoF/s", "cores": len(os.sched_getaffinity(0)),
+            "kind": kind, "cpu_model": _cpu_model(),
+            "sample": f"{what}: LevelSmoother.smooth on the full {'x'.join(map(str, dims))}-cell "
+                      f"level, best of {len(times)} (setup {step.setup_s:.1f} s excluded)"}
 
 
 def run_ours(args, cfg):
@@ -226,7 +312,7 @@ def run_ours(args, cfg):
     d, nc, k, kind, omega = cfg["d"], cfg["nc"], cfg["k"], cfg["kind"], cfg["omega"]
     if slab and args.config != 5:
         raise SystemExit("multi-GPU (slab) runs use the cfg-5 weak-scaling workload")
-    dims = (nc,) * d if not slab else (nc, nc, nc * ws)
+    dims = _bench_dims(cfg, ws, slab)
 
     if not slab:
         lvl = dg.build_hierarchy(d, nc, 0).levels[0]
@@ -392,7 +478,7 @@ def run_ours(args, cfg):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu = cpu_baseline_sample(cfg, args.config)
+        cpu = cpu_baseline_sample(cfg, dims)
 
     if rank == 0:
         step_roof_ms = max(flops_step / (peak * 1e12), bytes_step / (hbm * 1e9)) * 1e3
@@ -401,11 +487,7 @@ def run_ours(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded uniform[-1,1] b, x0)",
-            "config": {"workload": cfg["name"], "dims": list(dims), "k": k, "kind": kind,
-                       "omega": omega, "global_dofs": n_global,
-                       "parallelism": f"slab{ws}" if slab else "single",
-                       "l2": "inputs larger than L2 (no flush)" if n_local * 8 > 126e6
-                       else "inputs smaller than L2"},
+            "config": config_dict(cfg, dims, ws, n_global, slab),
             "roofline": {"bound": "tensor", "pipe": "fp64 (DFMA/DMMA)", "kernel": dom,
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak,
@@ -433,14 +515,21 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 50; 3 for --impl reference)")
+    ap.add_argument("--warmup", type=int, default=None,
+                    help="untimed warm-up steps (default 5; 1 for --impl reference)")
     ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--slab", action="store_true",
                     help="run the multi-GPU slab code path even on one GPU (validation)")
     args = ap.parse_args()
+    ref = args.impl == "reference"
+    if args.steps is None:
+        args.steps = 3 if ref else 50
+    if args.warmup is None:
+        args.warmup = 1 if ref else 5
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     cfg = CONFIGS[args.config]

@@ -74,6 +74,9 @@ class Staged:
             self.host.view(-1).copy_(self.dev)
             return
         if self.host is not None:
+            # in place like the reference, also on non-contiguous views;
+            # a read-only array raises as numpy's in-place update would
+            if not self.host.flags.writeable:
+                raise ValueError("assignment destination is read-only")
             out = self.dev.cpu().numpy()
-            if self.host.flags.writeable:
-                np.copyto(self.host.reshape(-1), out)
+            np.copyto(self.host, out.reshape(self.host.shape))

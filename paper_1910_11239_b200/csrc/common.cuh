@@ -38,9 +38,28 @@ struct Geo {
   FastDiv fv[3];   // division by nc[t] - 1 (patch vertex span)
 };
 
-// packed coordinates of list entries: x | y << 10 | z << 20 (global)
+// packed global coordinates of list entries: 3D x | y << 10 | z << 20
+// (<= 1024 cells per direction), 2D x | y << 15 (<= 32768); dg_level_create
+// rejects larger levels
+constexpr int kPackMax3 = 1024;
+constexpr int kPackMax2 = 32768;
 __host__ __device__ __forceinline__ int32_t pack3(int a, int b, int c) {
   return a | (b << 10) | (c << 20);
+}
+__host__ __device__ __forceinline__ int32_t pack_d(int d, int a, int b, int c) {
+  return d == 3 ? pack3(a, b, c) : (a | (b << 15));
+}
+template <int D>
+__host__ __device__ __forceinline__ void unpack_d(int e, int* v) {
+  if (D == 3) {
+    v[0] = e & 1023;
+    v[1] = (e >> 10) & 1023;
+    v[2] = (e >> 20) & 1023;
+  } else {
+    v[0] = e & 32767;
+    v[1] = (e >> 15) & 32767;
+    v[2] = 0;
+  }
 }
 
 template <int D, int N>
@@ -112,9 +131,7 @@ __device__ __forceinline__ void subdomain_info(const Geo& g, int id, bool packed
   if (PATCH) {
     int v[3] = {1, 1, 1};
     if (packed) {
-      v[0] = id & 1023;
-      v[1] = (id >> 10) & 1023;
-      v[2] = (id >> 20) & 1023;
+      unpack_d<D>(id, v);
     } else {
       uint32_t rem = (uint32_t)id;
 #pragma unroll
@@ -131,9 +148,7 @@ __device__ __forceinline__ void subdomain_info(const Geo& g, int id, bool packed
     }
   } else {
     if (packed) {
-      base[0] = id & 1023;
-      base[1] = (id >> 10) & 1023;
-      base[2] = (id >> 20) & 1023;
+      unpack_d<D>(id, base);
     } else {
       cell_multi<D>(g, id, base);
     }

@@ -240,7 +240,7 @@ static int build_flow(dg_level* L) {
         half += v[t] / 2;
       }
       const int col = parq * 2 + (half & 1);
-      pc[col].push_back(pack3(v[0], v[1], d == 3 ? v[2] : 0));
+      pc[col].push_back(pack_d(d, v[0], v[1], d == 3 ? v[2] : 0));
       lo[col] = std::min(lo[col], v[d - 1] - 1);
       hi[col] = std::max(hi[col], v[d - 1]);
     }
@@ -384,6 +384,17 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     return fail(DG_EUNSUPPORTED, "device path supports 1 <= degree <= 15");
   for (int t = 0; t < d; ++t)
     if (desc->ncells[t] < 1) return fail(DG_EINVAL, "ncells must be >= 1");
+  // packed colour lists hold global coordinates in 10 (3D) / 15 (2D) bits,
+  // and cell ids are 32-bit
+  for (int t = 0; t < d; ++t)
+    if (desc->ncells[t] > (d == 3 ? kPackMax3 : kPackMax2))
+      return fail(DG_EUNSUPPORTED, d == 3 ? "device path supports at most 1024 cells per direction in 3D"
+                                          : "device path supports at most 32768 cells per direction in 2D");
+  {
+    int64_t cells = 1;
+    for (int t = 0; t < d; ++t) cells *= desc->ncells[t];
+    if (cells >= (int64_t(1) << 31)) return fail(DG_EUNSUPPORTED, "more than 2^31 cells");
+  }
   const int last = desc->ncells[d - 1];
   if (desc->z_begin < 0 || desc->z_count < 1 || desc->z_begin + desc->z_count > last)
     return fail(DG_EINVAL, "stored window outside the level");
@@ -490,7 +501,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
         cc3[t] = (int)ct;
       }
       col[s & 1].push_back((int32_t)id);
-      colp[s & 1].push_back(pack3(cc3[0], cc3[1], cc3[2]));
+      colp[s & 1].push_back(pack_d(d, cc3[0], cc3[1], cc3[2]));
     }
     for (int k = 0; k < 2; ++k) {
       if (col[k].empty()) continue;
@@ -531,12 +542,12 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
         }
         const int col = parq * 2 + (half & 1);
         pc[col].push_back((int32_t)id);
-        pcp[col].push_back(pack3(v[0], v[1], d == 3 ? v[2] : 0));
+        pcp[col].push_back(pack_d(d, v[0], v[1], d == 3 ? v[2] : 0));
         for (int s = 0; s < (1 << d); ++s) {
           int c[3] = {0, 0, 0};
           for (int t = 0; t < d; ++t) c[t] = v[t] - 1 + ((s >> t) & 1);
           cc[col].push_back(local_of(c));
-          ccp[col].push_back(pack3(c[0], c[1], c[2]));
+          ccp[col].push_back(pack_d(d, c[0], c[1], c[2]));
         }
       }
     }
@@ -578,7 +589,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
           std::vector<int32_t> lst;
           for (int k = 2 * q; k <= 2 * q + 1; ++k)
             for (int32_t e : pcp[k]) {
-              const int vl = (d == 3) ? (e >> 20) & 1023 : (e >> 10) & 1023;
+              const int vl = (d == 3) ? (e >> 20) & 1023 : (e >> 15) & 32767;
               if (W <= 0 || (vl - 1) / W == w0 + w) lst.push_back(e);
             }
           if (lst.empty()) continue;
@@ -622,7 +633,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
             if (zhi < vlo || zlo > vhi) continue;
             int col = 0;
             for (int t = 0; t < d; ++t) col |= (a[t] & 1) << t;
-            cl[col].push_back(pack3(2 * a[0] + 1, 2 * a[1] + 1, d == 3 ? 2 * a[2] + 1 : 0));
+            cl[col].push_back(pack_d(d, 2 * a[0] + 1, 2 * a[1] + 1, d == 3 ? 2 * a[2] + 1 : 0));
           }
       for (int k = 0; k < ncl; ++k) {
         if (cl[k].empty()) continue;

@@ -514,7 +514,8 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
       int id = list ? list[idx] : (int)(start + idx);
       if (PATCH && delta >= 0) {
         // cluster mode: list holds packed base vertices of 2^d-patch clusters
-        int v[3] = {id & 1023, (id >> 10) & 1023, (id >> 20) & 1023};
+        int v[3];
+        unpack_d<D>(id, v);
         bool ok = true;
 #pragma unroll
         for (int t = 0; t < D; ++t) {
@@ -523,7 +524,7 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
         }
         ok = ok && v[D - 1] >= p.pv_lo && v[D - 1] <= p.pv_hi;
         inf[7] = ok;
-        id = pack3(v[0], v[1], D == 3 ? v[2] : 0);
+        id = pack_d(D, v[0], v[1], D == 3 ? v[2] : 0);
       }
       if (inf[7]) subdomain_info<D, PATCH>(p.geo, id, packed != 0, digit, base);
     }

@@ -96,9 +96,7 @@ __device__ __forceinline__ int res_cell(const Geo& geo, const int32_t* list, int
   if (list) {
     const int e = list[idx];
     if (packed) {
-      c[0] = e & 1023;
-      c[1] = (e >> 10) & 1023;
-      c[2] = (e >> 20) & 1023;
+      unpack_d<D>(e, c);
       return cell_local<D>(geo, c);
     }
     cell_multi<D>(geo, e, c);

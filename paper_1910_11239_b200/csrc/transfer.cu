@@ -629,7 +629,10 @@ static int launch_transfer(int dir, int accumulate, const double* e0, const doub
     // measured at Q5 32^3 -> 64^3: bulk prolongate 0.114 ms (plain stores
     // 0.115), bulk prolongate-accumulate 0.161 ms (load-add-store 0.191);
     // restriction reads faster through the LSU (0.098 vs 0.105 ms bulk)
-    if (env_int("DGB_TRANSFER_BULK", 1) && (dir == 0 || env_int("DGB_RESTRICT_BULK", 0))) {
+    // the bulk copies need 16-byte aligned cell rows: a misaligned view takes
+    // the LSU kernels below instead of faulting
+    const bool al16 = (((uintptr_t)src | (uintptr_t)dst) & 15) == 0;
+    if (al16 && env_int("DGB_TRANSFER_BULK", 1) && (dir == 0 || env_int("DGB_RESTRICT_BULK", 0))) {
       const size_t sm = TBulk<D, N>::SMEM;
       if (dir == 0) {
         auto k = accumulate ? prolong_bulk_kernel<D, N, true> : prolong_bulk_kernel<D, N, false>;

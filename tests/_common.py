@@ -61,3 +61,21 @@ def rhs_f(x):
 def rhs_g(x):
     """Dirichlet data of the compute_rhs fixtures."""
     return x[:, 0] ** 2 - 0.5 * x[:, -1] + 0.125
+
+
+REF_INSTALLED = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                             "baseline", "_ref")
+
+
+def ref_dgmg():
+    """The unmodified reference package `dgmg`: the copy `build()` installs
+    into baseline/_ref (it travels to the GPU box), else the source tree in
+    this container; None when neither exists.  Tests only (the checker)."""
+    import importlib
+    import sys
+    for path in (REF_INSTALLED, REF_SRC):
+        if os.path.isdir(os.path.join(path, "dgmg")):
+            if path not in sys.path:
+                sys.path.insert(0, path)
+            return importlib.import_module("dgmg")
+    return None

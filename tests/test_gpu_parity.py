@@ -129,6 +129,35 @@ def test_smoothing_step_matches_oracle_at_size(kind, d, nc, k, omega):
     assert rel(got - x0, want - x0) <= 1e-11
 
 
+@pytest.mark.parametrize("seed", [0, 1])
+def test_full_cfg5_avs_step_matches_oracle(seed):
+    """cfg 5 at the size bench.py times it (3D Q5, 64^3 cells, 56.6M DoFs, AVS
+    omega 1/4, the default one-launch bulk reduce-add path) against the CPU
+    oracle (~30-60 s of host work per seed)."""
+    ctx, _, sm = _setup(3, 64, 5, "avs", 0.25)
+    x0, b = inputs(ctx.ndofs, seed)
+    x = torch.from_numpy(x0).cuda()
+    sm.smooth(x, torch.from_numpy(b).cuda())
+    got = x.cpu().numpy()
+    del x
+    want = OracleLevel((64,) * 3, 5).smooth("avs", 0.25, x0, b)
+    assert rel(got, want) <= RTOL
+    assert rel(got - x0, want - x0) <= 1e-11
+
+
+def test_full_cfg3_mvs_sweep_matches_oracle():
+    """cfg 3 at the size bench.py times it (3D Q7, 32^3 cells, 16.8M DoFs, one
+    MVS sweep over 16 colours, omega 1) against the CPU oracle."""
+    ctx, _, sm = _setup(3, 32, 7, "mvs", 1.0)
+    x0, b = inputs(ctx.ndofs, 0)
+    x = torch.from_numpy(x0).cuda()
+    sm.smooth(x, torch.from_numpy(b).cuda())
+    got = x.cpu().numpy()
+    want = OracleLevel((32,) * 3, 7).smooth("mvs", 1.0, x0, b)
+    assert rel(got, want) <= RTOL
+    assert rel(got - x0, want - x0) <= 1e-11
+
+
 def test_mvs_full_cfg3_last_colour_local_residuals_vanish():
     """cfg 3 at full size (3D Q7, 32^3, 16 colours, omega=1): after the sweep,
     R_j (b - A x) = 0 on every patch of the last colour (exact local solves)."""
@@ -431,17 +460,19 @@ def test_host_pipelined_step_matches_device_step(kind, omega, k):
 
 
 @pytest.mark.parametrize("kind,omega", [("acs", 0.7), ("avs", 0.25)])
-@pytest.mark.parametrize("head,tail,layers", [(4, 4, 4), (2, 6, 6), (0, 8, 2)])
-def test_host_pipelined_uneven_chunks(kind, omega, head, tail, layers, monkeypatch):
+@pytest.mark.parametrize("head,tail,layers,nc", [(4, 4, 4, 24), (2, 6, 6, 24), (0, 8, 2, 24),
+                                                  (0, 2, 4, 11), (0, 4, 4, 17)])
+def test_host_pipelined_uneven_chunks(kind, omega, head, tail, layers, nc, monkeypatch):
     """2-layer head / tail chunks around the uniform ones (DGB_PIPE_HEAD /
-    DGB_PIPE_TAIL / DGB_PIPE_LAYERS): same result as the device step."""
+    DGB_PIPE_TAIL / DGB_PIPE_LAYERS): same result as the device step.  Odd
+    nz (11, 17) would leave a 1-layer chunk before the tail, which the
+    bounds merge away."""
     monkeypatch.setenv("DGB_PIPE_HEAD", str(head))
     monkeypatch.setenv("DGB_PIPE_TAIL", str(tail))
     monkeypatch.setenv("DGB_PIPE_LAYERS", str(layers))
-    nc = 24
     ctx, _, sm = _setup(3, nc, 2, kind, omega)
     bounds = sm._pipe_bounds(nc)
-    assert bounds[0] == 0 and bounds[-1] == nc and all(b > a for a, b in zip(bounds, bounds[1:]))
+    assert bounds[0] == 0 and bounds[-1] == nc and all(b - a >= 2 for a, b in zip(bounds, bounds[1:]))
     x0, b = inputs(ctx.ndofs, 15)
     assert sm._pipelinable(x0, b)
     xd = torch.from_numpy(x0).cuda()
@@ -500,3 +531,22 @@ def test_local_solver_apply_inverse_is_exact_local_solve():
         assert rel(pset.local_solver(j).apply_inverse(r), want) <= 1e-12
     with pytest.raises(ValueError):
         cset.local_solver(0).apply_inverse(np.zeros(5))
+
+
+def test_numpy_views_update_in_place_and_readonly_raises():
+    """x may be a non-contiguous numpy view (updated in place, like the
+    reference's in-place numpy arithmetic); a read-only x raises instead of
+    silently dropping the update."""
+    ctx, _, sm = _setup(3, 3, 2, "mvs", 1.0)
+    x0, b = inputs(ctx.ndofs, 21)
+    want = x0.copy()
+    sm.smooth(want, b)
+    big = np.zeros(2 * ctx.ndofs)
+    view = big[::2]
+    view[:] = x0
+    sm.smooth(view, b)
+    assert np.array_equal(big[::2], want) and not big[1::2].any()
+    ro = x0.copy()
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        sm.smooth(ro, b)

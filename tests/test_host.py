@@ -64,6 +64,37 @@ def test_library_rejects_bad_arguments_without_gpu():
         _lib.check(_lib.DG_ESINGULAR)
 
 
+@pytest.mark.parametrize("d,nc", [(3, (1025, 4, 4)), (3, (4, 4, 2048)), (2, (32769, 2, 1))])
+def test_level_create_rejects_levels_the_packed_lists_cannot_hold(d, nc):
+    """Colour lists pack global coordinates in 10 (3D) / 15 (2D) bits: larger
+    levels are refused before any allocation."""
+    from paper_1910_11239_b200 import _lib
+    lib = _lib.load()
+    desc = _lib.LevelDesc()
+    desc.dim, desc.degree = d, 1
+    for t in range(3):
+        desc.ncells[t] = nc[t]
+    desc.z_begin, desc.z_count = 0, nc[d - 1]
+    h = ctypes.c_void_p()
+    rc = lib.dg_level_create(ctypes.byref(desc), ctypes.byref(_lib.Tables()), ctypes.byref(h))
+    assert rc == _lib.DG_EUNSUPPORTED
+    assert b"cells per direction" in lib.dg_last_error()
+
+
+@pytest.mark.parametrize("starts,nz,want", [
+    ([0, 4, 8, 9], 11, [0, 4, 8, 11]),          # ..., 1-layer chunk, 2-layer tail
+    ([0, 8, 16, 17, 19], 21, [0, 8, 16, 19, 21]),
+    ([0, 4, 8, 12], 13, [0, 4, 8, 13]),         # 1-layer last chunk
+    ([0, 2, 4], 6, [0, 2, 4, 6]),
+    ([0], 3, [0, 3]),
+])
+def test_pipeline_chunks_are_at_least_two_layers(starts, nz, want):
+    from paper_1910_11239_b200.smoothers import _min2_chunks
+    got = _min2_chunks(starts, nz)
+    assert got == want
+    assert all(b - a >= 2 for a, b in zip(got, got[1:]))
+
+
 # --------------------------------------------------------------- 1D setup --
 @pytest.mark.parametrize("k", [1, 2, 3, 5, 7, 15])
 def test_host_1d_factors_match_reference(k):
