@@ -160,6 +160,14 @@ int64_t dg_last_launch_count(const dg_level_t* lvl);
  * 0 if it runs as one residual launch plus one launch per colour.           */
 int dg_flow_enabled(const dg_level_t* lvl);
 
+/* Bit mask of optional code compiled into this library:
+ * DG_BUILD_EXPERIMENTAL = the measured-and-rejected variants of DESIGN.md
+ * section 8 (dataflow step DGB_FLOW, clusters DGB_CLUSTER, z-windowed and
+ * overlapped AVS DGB_AVS_WIN / DGB_AVS_OVERLAP, persistent solves DGB_FDM=5/6,
+ * DMMA solves DGB_MMA), built only with -DDGB_EXPERIMENTAL.                 */
+#define DG_BUILD_EXPERIMENTAL 1
+int dg_build_flags(void);
+
 
 /* Nested-level transfers between a coarse level with coarse_cells[t] cells
  * per direction and its uniform refinement (2*coarse_cells[t]); e0, e1 are

@@ -26,6 +26,7 @@ EXPORTS = (
     "dg_level_ndofs", "dg_apply", "dg_residual", "dg_residual_cells",
     "dg_cell_fdm", "dg_patch_fdm", "dg_num_colours", "dg_colour_list",
     "dg_patch_gather_map", "dg_smooth", "dg_last_launch_count", "dg_flow_enabled",
+    "dg_build_flags",
     "dg_prolongate", "dg_restrict", "dg_cg_update", "dg_xpby", "dg_dot", "dg_solve_range",
     "dg_dist_apply", "dg_dist_cell_fdm",
 )
@@ -87,6 +88,7 @@ def load() -> ctypes.CDLL:
         "dg_smooth": ([vp, c_int, c_double, c_int, vp, vp, vp, c_int, vp], c_int),
         "dg_last_launch_count": ([vp], i64),
         "dg_flow_enabled": ([vp], c_int),
+        "dg_build_flags": ([], c_int),
         "dg_prolongate": ([c_int, c_int, ctypes.POINTER(c_int), _dp, _dp, vp, vp, c_int, vp],
                           c_int),
         "dg_restrict": ([c_int, c_int, ctypes.POINTER(c_int), _dp, _dp, vp, vp, vp], c_int),

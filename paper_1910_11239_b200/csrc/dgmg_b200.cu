@@ -10,7 +10,9 @@
 //    131-166), captured once into CUDA graphs and replayed.
 #include "../../include/dgmg_b200.h"
 #include "launch.h"
+#ifdef DGB_EXPERIMENTAL
 #include "flow.cuh"
+#endif
 
 #include <cstdlib>
 
@@ -79,9 +81,10 @@ struct GraphKey {
   const void* x;
   const void* b;
   const void* r;
+  uint64_t switches;  // switch_signature() at capture: a changed DGB_* variable re-captures
   bool operator<(const GraphKey& o) const {
-    return std::tie(kind, omega, reverse, x, b, r) <
-           std::tie(o.kind, o.omega, o.reverse, o.x, o.b, o.r);
+    return std::tie(kind, omega, reverse, x, b, r, switches) <
+           std::tie(o.kind, o.omega, o.reverse, o.x, o.b, o.r, o.switches);
   }
 };
 
@@ -201,6 +204,7 @@ static int check_layers(const dg_level* L, int z0, int z1) {
 // layers, colour skew `skew` between consecutive blocks.
 // ---------------------------------------------------------------------------
 
+#ifdef DGB_EXPERIMENTAL
 static int build_flow(dg_level* L) {
   int gp = 0, gr = 0;
   if (!L->has_patch || !flow_shape(L->d, L->n, &gp, &gr)) return DG_OK;
@@ -366,6 +370,20 @@ static int build_flow(dg_level* L) {
   f.units = units;
   L->flow_ok = true;
   return DG_OK;
+}
+
+#endif  // DGB_EXPERIMENTAL
+
+extern char** environ;
+
+uint64_t dgb::switch_signature() {
+  uint64_t h = 1469598103934665603ull;
+  for (char** e = environ; e && *e; ++e) {
+    if (std::strncmp(*e, "DGB_", 4) != 0) continue;
+    for (const char* c = *e; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;
+    h = (h ^ 0xff) * 1099511628211ull;
+  }
+  return h;
 }
 
 extern "C" {
@@ -578,7 +596,9 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     // launches; only dofs of a window's boundary layer see their updates in
     // (window, class) order instead (rounding-level difference, identical on
     // every slab decomposition because the windows are global).
+#ifdef DGB_EXPERIMENTAL
     L->avs_win = std::max(0, env_int("DGB_AVS_WIN", 0));
+#endif
     {
       const int W = L->avs_win;
       const int nq = 1 << d;
@@ -613,6 +633,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
       if (rc) { free_level(L); return rc; }
     }
   }
+#ifdef DGB_EXPERIMENTAL
   // 2^d-patch clusters for the additive step (cluster_kernel): base vertex
   // v0 = 2a+1 per direction, colour = parity of a; only clusters with a patch
   // vertex in [pv_begin, pv_end] along the last direction
@@ -644,6 +665,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
       }
     }
   }
+#endif  // DGB_EXPERIMENTAL
   if (desc->own_begin < zb || desc->own_end > zb + desc->z_count ||
       desc->own_begin > desc->own_end) {
     free_level(L);
@@ -653,10 +675,12 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     free_level(L);
     return rc;
   }
+#ifdef DGB_EXPERIMENTAL
   if (int rc = build_flow(L)) {
     free_level(L);
     return rc;
   }
+#endif
   {
     // the capture stream carries the patch solves at the highest priority;
     // the residual chunks of the overlapped AVS step run on `side` at the
@@ -872,6 +896,7 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
     }
     case DG_AVS: {
       if (!L->has_patch) return fail(DG_EUNSUPPORTED, "vertex patches unsupported here");
+#ifdef DGB_EXPERIMENTAL
       if (L->flow_ok && env_int("DGB_FLOW", 0)) {
         ++*nl;
         ResArgs ra = res_params(L, x, b, r);
@@ -879,9 +904,11 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
         return dispatch_flow(L->d, L->n, ra, fa, L->hres(), L->hpz.data(), L->hpzt.data(),
                              L->peo(), L->flow, st);
       }
+#endif
       const int64_t pdofs = L->pall_pk.count * (L->d == 3 ? (int64_t)L->m * L->m * L->m
                                                           : (int64_t)L->m * L->m);
       const int64_t amax = (int64_t)env_int("DGB_AVS_ATOMIC_MAX_MDOFS", 1 << 30) * 1000000;
+#ifdef DGB_EXPERIMENTAL
       if (env_int("DGB_AVS_ATOMIC", 1) && L->pall_pk.count > 0 && pdofs <= amax &&
           L->d == 3 && env_int("DGB_AVS_OVERLAP", 0)) {
         // residual and solves overlapped in z-chunks of C cell layers on two
@@ -955,6 +982,7 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
           return DG_OK;
         }
       }
+#endif  // DGB_EXPERIMENTAL
       if ((rc = res_range())) return rc;
       // default: one launch over all patches in spatial order; the overlaps
       // accumulate by the TMA engine's fp64 bulk reduce-add at L2 (atomic per
@@ -974,6 +1002,7 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
         p.atomic = 1;
         return dispatch_patch_fdm(L->d, L->n, p, L->hpz.data(), L->hpzt.data(), L->peo(), st);
       }
+#ifdef DGB_EXPERIMENTAL
       if (env_int("DGB_CLUSTER", 0) && !L->clus_pk.empty()) {
         for (auto& c : L->clus_pk) {
           ++*nl;
@@ -989,6 +1018,7 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
         }
         return DG_OK;
       }
+#endif  // DGB_EXPERIMENTAL
       const auto& order = env_int("DGB_AVS_COLOURS", 0) ? L->pcol_pk : L->pwin_pk;
       for (auto& c : order) {
         ++*nl;
@@ -1027,7 +1057,7 @@ int dg_smooth(dg_level_t* L, int kind, double omega, int reverse, double* x, con
   if (r == x || r == b) return fail(DG_EINVAL, "scratch residual must not alias x or b");
   cudaStream_t st = (cudaStream_t)stream;
   if (!use_graph) return smooth_launches(L, kind, omega, reverse, x, b, r, st, &L->last_launches);
-  GraphKey key{kind, omega, reverse ? 1 : 0, x, b, r};
+  GraphKey key{kind, omega, reverse ? 1 : 0, x, b, r, switch_signature()};
   auto it = L->graphs.find(key);
   if (it == L->graphs.end()) {
     if (L->graphs.size() >= 32) {
@@ -1058,7 +1088,20 @@ int dg_smooth(dg_level_t* L, int kind, double omega, int reverse, double* x, con
 int64_t dg_last_launch_count(const dg_level_t* L) { return L ? L->last_launches : -1; }
 
 int dg_flow_enabled(const dg_level_t* L) {
+#ifdef DGB_EXPERIMENTAL
   return L && L->flow_ok && env_int("DGB_FLOW", 0) ? 1 : 0;
+#else
+  (void)L;
+  return 0;
+#endif
+}
+
+int dg_build_flags(void) {
+#ifdef DGB_EXPERIMENTAL
+  return DG_BUILD_EXPERIMENTAL;
+#else
+  return 0;
+#endif
 }
 
 }  // extern "C"

@@ -58,6 +58,10 @@ inline int env_int(const char* name, int dflt) {
   return e && *e ? std::atoi(e) : dflt;
 }
 
+// FNV-1a hash of every DGB_* environment entry: part of the CUDA-graph cache
+// key, so a run-time switch flipped after a capture takes effect
+uint64_t switch_signature();
+
 template <typename K>
 inline int resident_ctas(K k, int threads, size_t smem, int* out) {
   int per_sm = 0, dev = 0, sms = 0;

@@ -3,7 +3,9 @@
 #pragma once
 #include "launch.h"
 #include "fdm2.cuh"
+#ifdef DGB_EXPERIMENTAL
 #include "fdm_mma.cuh"
+#endif
 
 #include <algorithm>
 #include <cstring>
@@ -34,6 +36,7 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
   p.pv_lo = q.pv_lo;
   p.pv_hi = q.pv_hi;
   p.direct = env_int("DGB_DIRECT", 2);
+#ifdef DGB_EXPERIMENTAL
   if constexpr (D == 3 && M % 8 == 0) {
     // fp64 tensor cores (fdm_mma.cuh) for m = 8, 16
     if (!q.cluster && q.zd && q.ztd && env_int("DGB_MMA", 0)) {
@@ -50,7 +53,9 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
       return DG_OK;
     }
   }
+#endif
   const int64_t ngroups = (q.count + G - 1) / G;
+#ifdef DGB_EXPERIMENTAL
   if (!q.atomic && !q.cluster && env_int("DGB_FDM", 2) == 5) {
     using S5 = Fdm5Shape<D, M, PATCH>;
     const size_t smem5 = sizeof(double) * S5::SMEM;
@@ -64,7 +69,9 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
     DG_CUDA(cudaGetLastError());
     return DG_OK;
   }
+#endif
   const size_t smem = sizeof(double) * fdm2_smem_doubles<D, M>();
+#ifdef DGB_EXPERIMENTAL
   if constexpr (PATCH) {
     if (q.cluster) {
       auto kc = cluster_kernel<D, M>;
@@ -93,6 +100,7 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
     DG_CUDA(cudaGetLastError());
     return DG_OK;
   }
+#endif
   if constexpr ((Rows<D, M, PATCH>::N % 2) == 0) {
     // the bulk reduce-add is an element-wise atomic fp64 add at L2, so the
     // bulk path also serves overlapping subdomains (atomic accumulation)

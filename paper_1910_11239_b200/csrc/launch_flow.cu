@@ -1,5 +1,6 @@
 // launch_flow.cu - dataflow AVS kernel (flow.cuh).
 #include "launch.h"
+#ifdef DGB_EXPERIMENTAL
 #include "flow.cuh"
 
 #include <algorithm>
@@ -91,3 +92,16 @@ int dispatch_flow(int d, int n, const ResArgs& ra, const FdmArgs& fa, const Host
 }
 
 }  // namespace dgb
+
+#else  // the dataflow step is a measured-and-rejected variant
+
+namespace dgb {
+bool flow_shape(int, int, int*, int*) { return false; }
+int dispatch_flow(int, int, const ResArgs&, const FdmArgs&, const HostRes&, const double*,
+                  const double*, const double*, const FlowDev&, cudaStream_t) {
+  return DG_EUNSUPPORTED;
+}
+}  // namespace dgb
+
+#endif  // DGB_EXPERIMENTAL
+
