@@ -415,6 +415,14 @@ def run_ours(args, cfg):
             traffic = json.load(f).get(f"cfg{args.config}")
     except (OSError, ValueError):
         traffic = None
+    # per-kernel fp64-pipe / issue / L1 utilisation of this config's step
+    # kernels from the committed ncu capture (profiles/ncu_pipes.json)
+    ncu_pipes = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_pipes.json")) as f:
+            ncu_pipes = json.load(f).get(f"cfg{args.config}")
+    except (OSError, ValueError):
+        ncu_pipes = None
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
@@ -468,6 +476,20 @@ def run_ours(args, cfg):
         del xd, bd, xsave
         e2e["copy_bound_ms"] = c_ms
         e2e["frac_of_copy_bound"] = c_ms / e_ms
+        # the reference's own callers pass pageable numpy arrays: the same
+        # call on those (the copies go through the driver's staging buffers)
+        xn, bn = x_h.copy(), b_h.copy()
+        sm.smooth(xn, bn)
+        torch.cuda.synchronize()
+        kp = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(kp):
+            sm.smooth(xn, bn)
+        p_ms = (time.perf_counter() - t0) * 1e3 / kp
+        e2e["pageable"] = {"value": n_global / (p_ms * 1e-3), "unit": "DoF/s", "ms_per_step": p_ms,
+                           "api": "LevelSmoother.smooth(numpy float64 arrays, pageable)",
+                           "timing": "host wall clock around the call (it returns with x final)"}
+        del xn, bn
     else:
         e2e = step_obj.e2e(x_h, b_h, reps=max(3, min(args.steps, 10)))
         e2e["value"] = e2e.pop("dofs_local") * ws / (e2e["ms_per_step"] * 1e-3)
@@ -499,6 +521,10 @@ def run_ours(args, cfg):
                          "even_odd": eo,
                          "peak_source": peak_src,
                          "step_frac": step_roof_ms / ms_step,
+                         "step_frac_executed": max(fx_step / (peak * 1e12),
+                                                   bytes_step / (hbm * 1e9)) * 1e3 / ms_step,
+                         "step_flops_executed": fx_step,
+                         "ncu_pipes": ncu_pipes,
                          "step_flops": flops_step, "step_bytes": bytes_step,
                          "hbm_peak_gbs": hbm, "hbm_source": hbm_src,
                          "kernel_ms": kt},

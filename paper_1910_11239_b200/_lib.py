@@ -15,7 +15,9 @@ import numpy as np
 from .tables import LevelTables, SingularLocalSolverError, device_tables
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdgmg_b200.so")
+# DGB_LIB selects another build of the same ABI (e.g. the experimental
+# variants, __graft_entry__.build() with DGB_EXPERIMENTAL=1)
+LIB_PATH = os.environ.get("DGB_LIB") or os.path.join(_HERE, "libdgmg_b200.so")
 
 DG_OK, DG_EINVAL, DG_ESINGULAR, DG_ECUDA, DG_EUNSUPPORTED = 0, 1, 2, 3, 4
 KINDS = {"acs": 0, "mcs": 1, "avs": 2, "mvs": 3}

@@ -68,14 +68,14 @@ struct Lay {
   static constexpr int F = (D == 3) ? N * N : N;               // fibers / tensor
   static constexpr int SZ = (D == 3) ? P * N * N : P * N;      // padded doubles
   static constexpr int NE = (D == 3) ? N * N * N : N * N;      // elements
-  __device__ __forceinline__ static int sstride(int t) {
+  __host__ __device__ __forceinline__ static int sstride(int t) {
     return t == 0 ? 1 : (t == 1 ? P : P * N);
   }
-  __device__ __forceinline__ static int gstride(int t) {
+  __host__ __device__ __forceinline__ static int gstride(int t) {
     return t == 0 ? 1 : (t == 1 ? N : N * N);
   }
   // shared-memory base offset of fiber f (0 <= f < F) along direction t
-  __device__ __forceinline__ static int sbase(int t, int f) {
+  __host__ __device__ __forceinline__ static int sbase(int t, int f) {
     if (D == 2) return t == 0 ? f * P : f;
     const int a = f % N, b = f / N;
     if (t == 0) return a * P + b * P * N;
@@ -83,7 +83,7 @@ struct Lay {
     return a + b * P;
   }
   // canonical (unpadded) base offset of fiber f along t
-  __device__ __forceinline__ static int gbase(int t, int f) {
+  __host__ __device__ __forceinline__ static int gbase(int t, int f) {
     if (D == 2) return t == 0 ? f * N : f;
     const int a = f % N, b = f / N;
     if (t == 0) return a * N + b * N * N;

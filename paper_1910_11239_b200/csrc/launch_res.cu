@@ -85,6 +85,19 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
       ngroups = (int64_t)((q.geo.nc[0] + 1) / 2) * ((q.geo.nc[1] + 1) / 2) * ((p.bnz + 1) / 2);
     }
   }
+#ifdef DGB_EXPERIMENTAL
+  if constexpr (D == 3 && N == 6) {
+    // narrow pitch (7 / 42): 4 CTAs per SM instead of 3, more bank conflicts
+    if (env_int("DGB_RES2_NARROW", 0)) {
+      const size_t smemn = sizeof(double) * res2_smem_doubles<D, N, true>();
+      auto kn = res2_kernel<D, N, true, 4>;
+      DG_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemn));
+      kn<<<(unsigned)ngroups, NT, smemn, st>>>(p);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
+  }
+#endif
   const size_t smem = sizeof(double) * res2_smem_doubles<D, N>();
   auto k = res2_kernel<D, N>;
   static bool attr = false;

@@ -56,7 +56,7 @@ struct Res2Params {
 // CTA across consecutive threads makes all three directions bank-conflict
 // free but scatters the neighbour-trace loads and row stores over 8 cells;
 // measured slower.)
-template <int D, int N, int G>
+template <int D, int N, int G, bool NARROW = false>
 struct RLay {
   using L = Lay<D, N>;
   static constexpr int F = L::F;
@@ -64,7 +64,7 @@ struct RLay {
   // the direction-1 fibers bank-conflict free as well (shared wavefronts per
   // cell group 504 -> 396, the residual is L1/shared-pipe bound); the
   // direction-2 fibers stay 2-way (no straight layout frees all three)
-  static constexpr bool WIDE = (D == 3 && N == 6);
+  static constexpr bool WIDE = (D == 3 && N == 6 && !NARROW);
   static constexpr int P = WIDE ? 9 : L::P;
   static constexpr int Q = WIDE ? 54 : L::P * N;
   static constexpr int GS = (D == 3) ? Q * N : L::SZ;
@@ -214,7 +214,7 @@ __device__ __forceinline__ void mass_fiber(const Res2Params<D, N>& p, int t, int
 
 // one group of G cells (work items grp*G .. grp*G+G-1 of the list/range);
 // all NT = G*F threads of the CTA take part; `sm` holds res_smem_doubles doubles.
-template <int D, int N, int G>
+template <int D, int N, int G, bool NARROW = false>
 __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32_t* list,
                                           int packed, int64_t start, int64_t count, int64_t grp,
                                           double* sm) {
@@ -245,7 +245,7 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
     }
   }
   __syncthreads();
-  using LY = RLay<D, N, G>;
+  using LY = RLay<D, N, G, NARROW>;
   constexpr int GS = LY::GS;
   constexpr int RPC = (D == 3) ? N * N : N;  // rows per cell
   for (int row = tid; row < G * RPC; row += NT) {
@@ -327,22 +327,23 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
   }
 }
 
-template <int D, int N>
-__global__ void __launch_bounds__(fdm2_groups<D, N>() * Lay<D, N>::F)
+template <int D, int N, bool NARROW = false, int MINB = 0>
+__global__ void __launch_bounds__(fdm2_groups<D, N>() * Lay<D, N>::F, MINB)
 res2_kernel(const __grid_constant__ Res2Params<D, N> p) {
   extern __shared__ __align__(16) double sm[];
-  res_group<D, N, fdm2_groups<D, N>()>(p, p.list, p.packed, p.start, p.count, blockIdx.x, sm);
+  res_group<D, N, fdm2_groups<D, N>(), NARROW>(p, p.list, p.packed, p.start, p.count, blockIdx.x,
+                                               sm);
 }
 
 
-template <int D, int N, int G>
+template <int D, int N, int G, bool NARROW = false>
 __host__ __device__ constexpr int res_smem_doubles() {
-  return 3 * G * RLay<D, N, G>::GS;
+  return 3 * G * RLay<D, N, G, NARROW>::GS;
 }
 
-template <int D, int N>
+template <int D, int N, bool NARROW = false>
 __host__ __device__ constexpr int res2_smem_doubles() {
-  return res_smem_doubles<D, N, fdm2_groups<D, N>()>();
+  return res_smem_doubles<D, N, fdm2_groups<D, N>(), NARROW>();
 }
 
 }  // namespace dgb

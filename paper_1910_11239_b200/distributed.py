@@ -197,9 +197,96 @@ class SlabSmoother:
                                       1, stream_handle()))
 
     def step(self) -> None:
-        """Ghost exchange then the local additive step (one per smoothing step)."""
+        """Ghost exchange and the local additive step (one per smoothing step).
+        On the device path with at least 6 owned layers the exchange runs on
+        its own stream and overlaps the interior work (`split_ranges`);
+        otherwise exchange, then the whole local step."""
+        if self._dev is not None and self.overlap_ok():
+            self._overlapped_step()
+            return
         halo_exchange(self.x, self.layout, self.group)
         self._local()
+
+    # ---- halo exchange overlapped with the interior ------------------------
+    def overlap_ok(self) -> bool:
+        """The split step needs an interior (>= 6 owned layers), neighbours to
+        wait for, and the overlap-safe update order (the default one-launch
+        bulk reduce-add path; the deterministic colour order keeps the plain
+        step)."""
+        import os
+        z0, z1 = self.layout.own
+        return (self.layout.world > 1 and z1 - z0 >= 6
+                and os.environ.get("DGB_SLAB_OVERLAP", "1") != "0"
+                and "0" not in (os.environ.get("DGB_AVS_ATOMIC", "1"),
+                                os.environ.get("DGB_AVS_ATOMIC_ORDER", "1")))
+
+    def split_ranges(self) -> dict:
+        """Layer ranges of the split step (global layer indices, half open).
+
+        interior (needs owned x only, so it runs while the halo is in flight):
+          residual on [z0+1, z1-1) (reads x on [z0, z1)); AVS patches with
+          vertex v_z in [z0+3, z1-2) (read r on [v-1, v], write x on
+          [z0+2, z1-3], layers no boundary residual reads) or ACS cells of
+          [z0+2, z1-2);
+        boundary (after the halo): residual on [z0-1, z0+1) and [z1-1, z1+1)
+          (reads x on [z0-2, z0+2) and [z1-2, z1+2)), then the remaining
+          patches v_z in [max(1,z0), z0+3) and [z1-2, min(nz-1,z1)+1), or
+          cells [z0, z0+2) and [z1-2, z1).
+        The union is exactly the plain step's work; the update order of a
+        DoF changes only by the reduce-add order (rounding)."""
+        z0, z1 = self.layout.own
+        nz = self.layout.nz
+        r_lo, r_hi = self.layout.res
+        if self.kind == "avs":
+            p_lo, p_hi = self.layout.pv[0], self.layout.pv[1] + 1
+            inner = (z0 + 3, z1 - 2)
+            outer = [(p_lo, inner[0]), (inner[1], p_hi)]
+        else:
+            inner = (z0 + 2, z1 - 2)
+            outer = [(z0, inner[0]), (inner[1], z1)]
+        return {"res_inner": (z0 + 1, z1 - 1),
+                "res_outer": [(r_lo, z0 + 1), (z1 - 1, min(nz, r_hi))],
+                "solve_inner": inner, "solve_outer": outer}
+
+    def _split_part(self, part: str) -> None:
+        from . import _lib
+        from ._device import stream_handle
+
+        dev = self._dev
+        lib = dev._lib
+        st = stream_handle()
+        kind = _lib.KINDS[self.kind]
+        rg = self.split_ranges()
+        xp, bp, rp = self.x.data_ptr(), self.b.data_ptr(), self.r.data_ptr()
+        if part == "interior":
+            res, sol = [rg["res_inner"]], [rg["solve_inner"]]
+        else:
+            res, sol = rg["res_outer"], rg["solve_outer"]
+        for lo, hi in res:
+            if hi > lo:
+                _lib.check(lib.dg_residual(dev.handle, xp, bp, rp, lo, hi, st))
+        for lo, hi in sol:
+            if hi > lo:
+                _lib.check(lib.dg_solve_range(dev.handle, kind, self.omega, rp, xp, lo, hi, st))
+
+    def _overlapped_step(self) -> None:
+        cur = torch.cuda.current_stream()
+        if not hasattr(self, "_comm"):
+            self._comm = torch.cuda.Stream()
+        comm = self._comm
+        comm.wait_stream(cur)  # the previous step's updates of the sent layers
+        plan = self.layout.halo_plan()
+        with torch.cuda.stream(comm):
+            ops = []
+            for peer, send, recv in plan:
+                ops.append(dist.P2POp(dist.isend, self.x[send], peer, self.group))
+                ops.append(dist.P2POp(dist.irecv, self.x[recv], peer, self.group))
+            works = dist.batch_isend_irecv(ops)
+        self._split_part("interior")
+        for w in works:
+            w.wait()          # the current stream waits for the exchange
+        cur.wait_stream(comm)
+        self._split_part("boundary")
 
     def owned_x(self) -> torch.Tensor:
         return self.x[self.owned]

@@ -131,3 +131,40 @@ def test_slab_layout_ranges():
     assert uneven == [(0, 4), (4, 7), (7, 10)]
     with pytest.raises(ValueError):
         SlabLayout((4, 4, 3), 1, 1, 2).validate()
+
+
+@pytest.mark.parametrize("nz,world,kind", [(24, 2, "avs"), (24, 3, "acs"), (40, 4, "avs"), (18, 3, "avs")])
+def test_split_ranges_cover_the_plain_step(nz, world, kind):
+    """SlabSmoother.split_ranges: interior + boundary residual layers = the
+    residual range, patch (or cell) ranges = the plain step's, and the
+    interior part reads no ghost layer and writes no layer a boundary
+    residual reads."""
+    for rank in range(world):
+        sm = SlabSmoother((4, 4, nz), 2, kind, 0.25 if kind == "avs" else 0.7, rank=rank,
+                          world=world, device="cpu", compute=lambda *a: None)
+        lay = sm.layout
+        z0, z1 = lay.own
+        rg = sm.split_ranges()
+        res = sorted([rg["res_inner"]] + rg["res_outer"])
+        cover = set()
+        for lo, hi in res:
+            cover |= set(range(lo, hi))
+        assert cover == set(range(*lay.res))
+        sol = sorted([rg["solve_inner"]] + rg["solve_outer"])
+        cover = set()
+        for lo, hi in sol:
+            assert not cover & set(range(lo, hi))
+            cover |= set(range(lo, hi))
+        want = set(range(lay.pv[0], lay.pv[1] + 1)) if kind == "avs" else set(range(z0, z1))
+        assert cover == want
+        # interior residual reads x on [lo-1, hi+1): owned layers only
+        lo, hi = rg["res_inner"]
+        assert lo - 1 >= z0 and hi + 1 <= z1
+        # interior writes vs boundary residual reads
+        slo, shi = rg["solve_inner"]
+        written = set(range(slo - 1, shi)) if kind == "avs" else set(range(slo, shi))
+        for blo, bhi in rg["res_outer"]:
+            assert not written & set(range(blo - 1, bhi + 1))
+        # interior solves read r only where the interior residual wrote it
+        read = set(range(slo - 1, shi)) if kind == "avs" else set(range(slo, shi))
+        assert read <= set(range(lo, hi))

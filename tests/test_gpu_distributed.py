@@ -124,3 +124,41 @@ def test_cfg5_slab_window_interface_patches(avs_atomic):
     got = _slab_run(dims, k, "avs", 0.25, world, 1, x0, b)
     single = _single_run(dims, k, "avs", 0.25, 1, x0, b)
     _check_single(got, single, x0, avs_atomic)
+
+
+@pytest.mark.parametrize("kind,world", [("avs", 2), ("avs", 3), ("acs", 2)])
+def test_split_step_equals_plain_step(kind, world):
+    """The halo-overlapped step (interior residual + solves while the halo is
+    in flight, then the boundary part; SlabSmoother.split_ranges) computes the
+    plain local step: equal to rounding (reduce-add order) on every rank,
+    and the oracle to 1e-12."""
+    dims, k = (6, 5, 8 * world), 2
+    omega = 0.25 if kind == "avs" else 0.7
+    n = int(np.prod(dims)) * (k + 1) ** 3
+    x0, b = inputs(n, 13)
+    plain = _slab_run(dims, k, kind, omega, world, 1, x0, b)
+    sms = [SlabSmoother(dims, k, kind, omega, rank=r, world=world, device="cuda")
+           for r in range(world)]
+    for sm in sms:
+        lay = sm.layout
+        w0 = lay.window[0] * lay.layer_dofs
+        own = sm.owned
+        sm.x[own].copy_(torch.from_numpy(x0[w0 + own.start:w0 + own.stop]))
+        sm.b[own].copy_(torch.from_numpy(b[w0 + own.start:w0 + own.stop]))
+    _exchange(sms, "b")
+    # interior before the exchange (it must not need the ghosts), boundary after
+    for sm in sms:
+        sm._split_part("interior")
+    _exchange(sms, "x")
+    for sm in sms:
+        sm._split_part("boundary")
+    torch.cuda.synchronize()
+    got = np.empty_like(x0)
+    for sm in sms:
+        lay = sm.layout
+        w0 = lay.window[0] * lay.layer_dofs
+        own = sm.owned
+        got[w0 + own.start:w0 + own.stop] = sm.owned_x().cpu().numpy()
+    assert rel(got - x0, plain - x0) <= 1e-14
+    want = OracleLevel(dims, k, h=1.0 / dims[0]).smooth(kind, omega, x0, b)
+    assert rel(got, want) <= 1e-12
