@@ -675,8 +675,6 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     free_level(L);
     return rc;
   }
-  prepare_cell_maps(d, n);
-  if (L->has_patch) prepare_patch_maps(d, n);
 #ifdef DGB_EXPERIMENTAL
   if (int rc = build_flow(L)) {
     free_level(L);

@@ -47,9 +47,6 @@ struct Fdm2Params {
   int eo;       // interior digit uses the even/odd halves
   int pv_lo, pv_hi;  // cluster mode: patch vertices v_d outside are skipped
   int direct;   // first/last contraction straight from/to global rows (no gather/scatter pass)
-  // thread -> (g << 16 | f) per pass kind (fibermap.h: 0 direction 0, 1 directions
-  // 1..d-2, 2 the fused direction d-1), 3 * G * F entries; nullptr = natural order
-  const uint32_t* maps;
   Geo geo;
   FdmMats<M> mats;
 };
@@ -544,19 +541,8 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
       s_cell[tid][s] = (int64_t)cell_local<D>(p.geo, c) * NEc;
     }
   }
-  // thread -> (subdomain, fiber) per pass kind (fibermap.h)
-  int g = tid / F, f = tid - (tid / F) * F;  // direction-0 passes
-  int g1 = g, f1 = f;                        // directions 1 .. d-2
-  constexpr bool IL = fdm_interleave<D, G>();
-  int gi = IL ? tid % G : g, fi = IL ? tid / G : f;  // fused direction d-1
-  if (p.maps && tid < NT) {
-    const uint32_t m0 = __ldg(p.maps + tid), m1 = __ldg(p.maps + NT + tid),
-                   m2 = __ldg(p.maps + 2 * NT + tid);
-    g = (int)(m0 >> 16), f = (int)(m0 & 0xffff);
-    g1 = (int)(m1 >> 16), f1 = (int)(m1 & 0xffff);
-    gi = (int)(m2 >> 16), fi = (int)(m2 & 0xffff);
-  }
   __syncthreads();
+  const int g = tid / F, f = tid - (tid / F) * F;
   const bool active = s_info[g][7];
   const int* dg = s_info[g];
   constexpr int GSZ = fdm_gstride<D, M, G>();
@@ -656,14 +642,15 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
   // forward contractions with Z^T, directions 1 .. D-2
 #pragma unroll
   for (int t = 1; t < D - 1; ++t) {
-    if (s_info[g1][7])
-      fdm_fiber<M, true>(p.mats, p.eo, s_info[g1][t], sm + g1 * GSZ, L::sbase(t, f1), L::sstride(t));
+    if (active) fdm_fiber<M, true>(p.mats, p.eo, dg[t], buf, L::sbase(t, f), L::sstride(t));
     __syncthreads();
   }
   // fused: Z^T along D-1, scale by 1/Lambda-sum, Z along D-1.  In 3D the
   // threads take the G subdomains interleaved here (with the group stride of
   // fdm_gstride the half-warp accesses of this strided pass are conflict free)
   {
+    constexpr bool IL = fdm_interleave<D, G>();
+    const int gi = IL ? tid % G : g, fi = IL ? tid / G : f;
     if (s_info[gi][7]) {
       constexpr int t = D - 1;
       const int* dgi = s_info[gi];
@@ -686,8 +673,7 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
 #pragma unroll
   for (int s = 0; s < D - 2; ++s) {
     const int t = D - 2 - s;
-    if (s_info[g1][7])
-      fdm_fiber<M, false>(p.mats, p.eo, s_info[g1][t], sm + g1 * GSZ, L::sbase(t, f1), L::sstride(t));
+    if (active) fdm_fiber<M, false>(p.mats, p.eo, dg[t], buf, L::sbase(t, f), L::sstride(t));
     __syncthreads();
   }
   if constexpr (BULK) {

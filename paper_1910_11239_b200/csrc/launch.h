@@ -100,10 +100,6 @@ int dispatch_cell_fdm(int d, int n, const FdmArgs& p, const double* hz, const do
                       const double* heo, cudaStream_t st);
 int dispatch_patch_fdm(int d, int n, const FdmArgs& p, const double* hz, const double* hzt,
                        const double* heo, cudaStream_t st);
-// fibermap.h thread maps of the bulk solve kernels of a level's shape (host,
-// outside any graph capture)
-void prepare_cell_maps(int d, int n);
-void prepare_patch_maps(int d, int n);
 bool flow_shape(int d, int n, int* gp, int* gr);
 int dispatch_flow(int d, int n, const ResArgs& ra, const FdmArgs& fa, const HostRes& h,
                   const double* hz, const double* hzt, const double* heo, const FlowDev& fd,

@@ -4,7 +4,6 @@
 #include "launch.h"
 #include "fdm2.cuh"
 #ifdef DGB_EXPERIMENTAL
-#include "fibermap.h"
 #include "fdm3.cuh"
 #endif
 #ifdef DGB_EXPERIMENTAL
@@ -12,83 +11,9 @@
 #endif
 
 #include <algorithm>
-#include <atomic>
 #include <cstring>
-#include <mutex>
 
 namespace dgb {
-
-#ifdef DGB_EXPERIMENTAL
-// fibermap.h maps of the bulk kernel's three pass kinds, built and uploaded
-// once per kernel shape by fdm_prepare_maps (dg_level_create: never inside a
-// graph capture); launches before that run in the natural order
-template <int D, int M, bool PATCH>
-static std::atomic<const uint32_t*>& fdm_maps_slot() {
-  static std::atomic<const uint32_t*> slot{nullptr};
-  return slot;
-}
-
-template <int D, int M, bool PATCH>
-static void fdm_prepare_maps() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    using L = Lay<D, M>;
-    using R = Rows<D, M, PATCH>;
-    constexpr int G = fdm2_groups<D, M>();
-    constexpr int F = L::F;
-    constexpr int N = R::N;
-    constexpr int NEc = (D == 3) ? N * N * N : N * N;
-    constexpr int GSZ = fdm_gstride<D, M, G>();
-    constexpr int H = PATCH ? 2 : 1;
-    // dense 16-byte rows: mapped where the rows are not a power-of-two number
-    // of chunks (those use the rotated chunk order of fdm2.cuh instead)
-    constexpr int NB = (N % 8 == 0) ? 0 : H;
-    std::vector<uint32_t> all;
-    for (int kind = 0; kind < 3; ++kind) {
-      const int t = kind == 0 ? 0 : (kind == 1 ? std::min(1, D - 1) : D - 1);
-      std::vector<FiberItem> items;
-      for (int g = 0; g < G; ++g)
-        for (int f = 0; f < F; ++f) {
-          FiberItem it;
-          it.code = (uint32_t)g << 16 | (uint32_t)f;
-          it.a = (g * GSZ + L::sbase(t, f)) % 16;
-          it.b[0] = it.b[1] = 0;
-          if (kind == 0) {
-            int slot0 = 0, goff = 0;
-            fiber_rows<D, M, PATCH>(f, slot0, goff);
-            for (int h = 0; h < NB; ++h)
-              it.b[h] = ((g * GSZ + dense_off<NEc>(slot0 + h) + goff) / 2) % 8;
-          }
-          items.push_back(it);
-        }
-      std::vector<uint32_t> m = fibermap_build(items, kind == 0 ? NB : 0);
-      if (kind == 2 && fdm_interleave<D, G>()) {
-        // keep the interleaved order when the builder does not beat it
-        std::vector<FiberItem> il(items.size());
-        for (int tid = 0; tid < G * F; ++tid) il[tid] = items[(tid % G) * F + tid / G];
-        std::vector<FiberItem> got(items.size());
-        for (size_t i = 0; i < m.size(); ++i) got[i] = items[(m[i] >> 16) * F + (m[i] & 0xffff)];
-        if (fibermap_cost(il, 0) <= fibermap_cost(got, 0))
-          for (size_t i = 0; i < m.size(); ++i) m[i] = il[i].code;
-      }
-      all.insert(all.end(), m.begin(), m.end());
-    }
-    uint32_t* d = nullptr;
-    if (cudaMalloc(&d, all.size() * sizeof(uint32_t)) != cudaSuccess) return;
-    // the pageable copy may still be in flight on the legacy stream when
-    // cudaMemcpy returns; a later capture on a blocking stream would then
-    // inherit an implicit dependency and be invalidated: wait for it here
-    if (cudaMemcpy(d, all.data(), all.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) !=
-            cudaSuccess ||
-        cudaDeviceSynchronize() != cudaSuccess) {
-      cudaFree(d);
-      return;
-    }
-    fdm_maps_slot<D, M, PATCH>().store(d);
-  });
-}
-
-#endif  // DGB_EXPERIMENTAL
 
 template <int D, int M, bool PATCH>
 static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, const double* heo,
@@ -114,7 +39,6 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
   p.pv_lo = q.pv_lo;
   p.pv_hi = q.pv_hi;
   p.direct = env_int("DGB_DIRECT", 2);
-  p.maps = nullptr;
 #ifdef DGB_EXPERIMENTAL
   if constexpr (D == 3 && M % 8 == 0) {
     // fp64 tensor cores (fdm_mma.cuh) for m = 8, 16
@@ -206,9 +130,6 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
     }
 #endif
     if (p.direct == 2 && (!q.atomic || env_int("DGB_BULK_ATOMIC", 1)) && !q.cluster) {
-#ifdef DGB_EXPERIMENTAL
-      if (env_int("DGB_FIBERMAP", 0)) p.maps = fdm_maps_slot<D, M, PATCH>().load();
-#endif
       auto kb = fdm2_kernel<D, M, PATCH, true>;
       static bool attr_b = false;
       if (!attr_b) {

@@ -13,17 +13,4 @@ int dispatch_cell_fdm(int d, int n, const FdmArgs& p, const double* hz,
                                    ", n " + std::to_string(n));
 }
 
-void prepare_cell_maps(int d, int n) {
-#ifdef DGB_EXPERIMENTAL
-  if (!env_int("DGB_FIBERMAP", 0)) return;
-#define X(D, N) if (d == D && n == N) { fdm_prepare_maps<D, N, false>(); return; }
-  DG_N_CASES(X, 2)
-  DG_N_CASES(X, 3)
-#undef X
-#else
-  (void)d;
-  (void)n;
-#endif
-}
-
 }  // namespace dgb

@@ -14,17 +14,4 @@ int dispatch_patch_fdm(int d, int n, const FdmArgs& p, const double* hz,
                                    " (vertex patches support k <= 7)");
 }
 
-void prepare_patch_maps(int d, int n) {
-#ifdef DGB_EXPERIMENTAL
-  if (!env_int("DGB_FIBERMAP", 0)) return;
-#define X(D, N) if (d == D && n == N) { fdm_prepare_maps<D, 2 * N, true>(); return; }
-  X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8)
-  X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 6) X(3, 7) X(3, 8)
-#undef X
-#else
-  (void)d;
-  (void)n;
-#endif
-}
-
 }  // namespace dgb

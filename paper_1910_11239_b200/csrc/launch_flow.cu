@@ -56,7 +56,6 @@ static int launch_flow(const ResArgs& ra, const FdmArgs& fa, const HostRes& h, c
   f.packed = 1;
   f.geo = fa.geo;
   f.direct = env_int("DGB_DIRECT", 1);
-  f.maps = nullptr;
   std::memcpy(f.mats.fwd, hz, sizeof(f.mats.fwd));
   std::memcpy(f.mats.bwd, hzt, sizeof(f.mats.bwd));
   f.eo = heo != nullptr;
