@@ -97,6 +97,7 @@ struct dg_level {
   const double *mass = nullptr, *adiag = nullptr, *bg = nullptr;
   const double *cz = nullptr, *czt = nullptr, *cinv = nullptr;
   const double *pz = nullptr, *pzt = nullptr, *pinv = nullptr;
+  const double *ceod = nullptr, *peod = nullptr;  // device even/odd tables (tensor-core solves)
   double alpha = 0, beta = 0, betap = 0;
   bool has_patch = false;
   std::vector<double> hcz, hczt, hpz, hpzt;  // host copies for the kernel parameter space
@@ -174,6 +175,7 @@ static FdmArgs fdm_params(const dg_level* L, bool patch, const double* r, double
   p.invsum = patch ? L->pinv : L->cinv;
   p.zd = patch ? L->pz : L->cz;
   p.ztd = patch ? L->pzt : L->czt;
+  p.eod = patch ? L->peod : L->ceod;
   p.omega = omega;
   p.geo = L->geo;
   return p;
@@ -463,6 +465,10 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     parts.push_back({T->patch_zt, 4 * m * m});
     parts.push_back({T->patch_invsum, pw * pe});
   }
+  const int ceo_at = (int)parts.size();
+  if (!L->hceo.empty()) parts.push_back({L->hceo.data(), (int64_t)L->hceo.size()});
+  const int peo_at = (int)parts.size();
+  if (!L->hpeo.empty()) parts.push_back({L->hpeo.data(), (int64_t)L->hpeo.size()});
   int64_t total = 0;
   for (auto& pr : parts) total += (pr.second + 1) & ~int64_t(1);
   cudaError_t e = cudaMalloc(&L->dtab, total * sizeof(double));
@@ -496,6 +502,8 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     L->pzt = dptr[7];
     L->pinv = dptr[8];
   }
+  if (!L->hceo.empty()) L->ceod = dptr[ceo_at];
+  if (!L->hpeo.empty()) L->peod = dptr[peo_at];
 
   // ---- colour lists -------------------------------------------------------
   const int* nc = desc->ncells;

@@ -49,6 +49,7 @@ struct FdmArgs {
   const double* invsum = nullptr;
   const double* zd = nullptr;   // device Z per digit (row-major m x m), tensor-core path
   const double* ztd = nullptr;  // device Z^T per digit
+  const double* eod = nullptr;  // device even/odd halves of the interior digit (4 tables)
   double omega = 0;
   Geo geo;
 };

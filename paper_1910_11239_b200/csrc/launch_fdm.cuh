@@ -4,6 +4,9 @@
 #include "launch.h"
 #include "fdm2.cuh"
 #ifdef DGB_EXPERIMENTAL
+#include "fdm4.cuh"
+#endif
+#ifdef DGB_EXPERIMENTAL
 #include "fdm3.cuh"
 #endif
 #ifdef DGB_EXPERIMENTAL
@@ -52,6 +55,26 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
         attr = true;
       }
       k<<<(unsigned)((q.count + S::GS - 1) / S::GS), S::NT, smem, st>>>(p, q.zd, q.ztd);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
+  }
+#endif
+#ifdef DGB_EXPERIMENTAL
+  if constexpr (D == 3 && M == 16) {
+    // tensor cores with the even/odd split (fdm4.cuh)
+    // measured at par with the DFMA kernel (cfg 3 solve 0.98 vs 0.95 ms, cfg 4
+    // 0.100 vs 0.087 ms; profiles/r02): opt-in
+    const int v4 = env_int("DGB_FDM4", 0);
+    if (!q.cluster && q.zd && q.ztd && v4) {
+      auto k4 = v4 == 2 ? fdm4_kernel<PATCH, 3> : fdm4_kernel<PATCH, 4>;
+      const size_t smem4 = sizeof(double) * Fdm4Lay<PATCH>::SZ;
+      static bool attr4[3] = {false, false, false};
+      if (!attr4[v4 & 3 ? (v4 == 2) : 0]) {
+        DG_CUDA(cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4));
+        attr4[v4 == 2] = true;
+      }
+      k4<<<(unsigned)q.count, Fdm4Lay<PATCH>::NT, smem4, st>>>(p, q.zd, q.ztd, p.eo ? q.eod : nullptr);
       DG_CUDA(cudaGetLastError());
       return DG_OK;
     }

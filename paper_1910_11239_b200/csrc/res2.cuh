@@ -107,22 +107,65 @@ __device__ __forceinline__ int res_cell(const Geo& geo, const int32_t* list, int
   return cell;
 }
 
+// face scalars of the global neighbour fiber f along t on side `right`
+// (a_pm x_R: hi = alpha x_R[0] + beta bg0.x_R, all = beta' x_R[0];
+//  a_pm^T x_L: hi = alpha x_L[n-1] + beta' bg1.x_L, all = beta x_L[n-1])
+template <int D, int N>
+__device__ __forceinline__ void face_pair(const Res2Params<D, N>& p, int t, int f, const int* c,
+                                          bool right, double& hi, double& all) {
+  using L = Lay<D, N>;
+  int nb[3] = {c[0], c[1], D == 3 ? c[2] : 0};
+  nb[t] += right ? 1 : -1;
+  const double* q = p.x + (int64_t)cell_local<D>(p.geo, nb) * L::NE + L::gbase(t, f);
+  double xv[N];
+  if (t == 0) {
+    row_load_reg<N>(xv, q);
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; ++k) xv[k] = __ldg(q + k * L::gstride(t));
+  }
+  double g = 0.0;
+  if (right) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) g = fma(p.mats.bg0[k], xv[k], g);
+    all = p.betap * xv[0];
+    hi = p.alpha * xv[0] + p.beta * g;
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; ++k) g = fma(p.mats.bg1[k], xv[k], g);
+    all = p.beta * xv[N - 1];
+    hi = p.alpha * xv[N - 1] + p.betap * g;
+  }
+}
+
 // G_t fiber: A_diag(digit) along t plus the rank-2 neighbour couplings.  The
 // neighbour fibers are reduced to their face value and normal derivative
 // before the own fiber is loaded, so at most one fiber-sized array of
-// neighbour data is live (register budget at n = 16).
+// neighbour data is live (register budget at n = 16).  `pre` (blocked mode)
+// carries the out-of-block side's scalars, loaded at kernel start.
+struct FacePre {
+  int side;  // -1 none, 0 left, 1 right
+  double hi, all;
+};
+
 template <int D, int N, class LY>
 __device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, int f,
                                              const int* c, const double* X, double* out,
                                              const double* XR = nullptr,
-                                             const double* XL = nullptr) {
+                                             const double* XL = nullptr,
+                                             const FacePre* pre = nullptr) {
   using L = Lay<D, N>;
   const int sb = LY::sbase(t, f), ss = LY::sstride(t);
   const int digit = (c[t] == 0 ? 1 : 0) | (c[t] == p.geo.nc[t] - 1 ? 2 : 0);
   const int gb = L::gbase(t, f), gs = L::gstride(t);
   int nb[3] = {c[0], c[1], D == 3 ? c[2] : 0};
   double r_hi = 0.0, r_all = 0.0, l_lo = 0.0, l_all = 0.0;
-  if (!(digit & 2)) {  // a_pm x_R: value and normal derivative at the shared face
+  if (pre && pre->side == 1) {
+    r_hi = pre->hi, r_all = pre->all;
+  } else if (pre && pre->side == 0) {
+    l_lo = pre->hi, l_all = pre->all;
+  }
+  if (!(digit & 2) && !(pre && pre->side == 1)) {  // a_pm x_R: value and normal derivative at the shared face
     double xr[N];
     if (XR) {  // neighbour tensor of the same CTA block (shared memory)
 #pragma unroll
@@ -143,7 +186,7 @@ __device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, i
     r_all = p.betap * xr[0];
     r_hi = p.alpha * xr[0] + p.beta * g;
   }
-  if (!(digit & 1)) {  // a_pm^T x_L
+  if (!(digit & 1) && !(pre && pre->side == 0)) {  // a_pm^T x_L
     double xl[N];
     if (XL) {
 #pragma unroll
@@ -248,6 +291,26 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
   using LY = RLay<D, N, G, NARROW>;
   constexpr int GS = LY::GS;
   constexpr int RPC = (D == 3) ? N * N : N;  // rows per cell
+  // blocked mode: every cell has one out-of-block face per direction (the
+  // side away from its block partner); its neighbour fiber comes from global
+  // memory.  Load those first and reduce them to their two face scalars, so
+  // their latency overlaps the block's row loads instead of stalling the
+  // contraction phases (ncu r02: long-scoreboard stalls 21%).
+  FacePre pre[D];
+  if constexpr (D == 3 && G == 8) {
+    if (blocked) {
+      const int g0 = tid / Lay<D, N>::F, f0 = tid - g0 * Lay<D, N>::F;
+      const int* cc = s_c[g0];
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        const bool right = (g0 >> t) & 1;  // high cell of the pair: +e_t is outside
+        const bool at_bnd = right ? cc[t] == p.geo.nc[t] - 1 : cc[t] == 0;
+        pre[t].side = (s_cell[g0] < 0 || at_bnd) ? -1 : (right ? 1 : 0);
+        pre[t].hi = pre[t].all = 0.0;
+        if (pre[t].side >= 0) face_pair<D, N>(p, t, f0, cc, right, pre[t].hi, pre[t].all);
+      }
+    }
+  }
   for (int row = tid; row < G * RPC; row += NT) {
     const int gg = row / RPC, w = row - gg * RPC;
     const int cell = s_cell[gg];
@@ -272,8 +335,13 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
     return s_cell[gn] >= 0 ? sm + gn * GS : nullptr;
   };
   __syncthreads();
-  if (act(0)) stiff2_fiber<D, N, LY>(p, 0, ft[0], s_c[gt[0]], X(0), A(0), nbr(0, true), nbr(0, false));
-  if (act(1)) stiff2_fiber<D, N, LY>(p, 1, ft[1], s_c[gt[1]], X(1), B(1), nbr(1, true), nbr(1, false));
+  const bool usepre = D == 3 && G == 8 && blocked;
+  if (act(0))
+    stiff2_fiber<D, N, LY>(p, 0, ft[0], s_c[gt[0]], X(0), A(0), nbr(0, true), nbr(0, false),
+                           usepre ? &pre[0] : nullptr);
+  if (act(1))
+    stiff2_fiber<D, N, LY>(p, 1, ft[1], s_c[gt[1]], X(1), B(1), nbr(1, true), nbr(1, false),
+                           usepre ? &pre[D > 1 ? 1 : 0] : nullptr);
   __syncthreads();
   if (act(1)) mass_fiber<D, N, false, LY>(p, 1, ft[1], A(1), nullptr);
   if (act(0)) mass_fiber<D, N, false, LY>(p, 0, ft[0], B(0), nullptr);
@@ -288,7 +356,7 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
     if (act(2)) {
       mass_fiber<D, N, true, LY>(p, 2, ft[2], A(2), B(2));  // A = M_2 (M_1 G_0 + M_0 G_1)
       stiff2_fiber<D, N, LY>(p, 2, ft[2], s_c[gt[2]], X(2), B(2), nbr(2, true),
-                             nbr(2, false));                 // B = G_2
+                             nbr(2, false), usepre ? &pre[D - 1] : nullptr);                 // B = G_2
     }
     __syncthreads();
     if (act(0) && p.b) row_load_reg<N>(bv, p.b + gi);
