@@ -299,8 +299,11 @@ def run_ours(args, cfg):
         # keep stdout to the one JSON line (NCCL prints its version otherwise)
         # (the image's Python starts with NCCL_DEBUG=VERSION, which prints the
         # version line on stdout: lower it, and send any NCCL log to stderr)
+        # NCCL's init lines (ranks, nranks, transports) go to stderr for the
+        # driver's log; an explicit NCCL_DEBUG setting is kept as given
         if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-            os.environ["NCCL_DEBUG"] = "WARN"
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if not dist.is_initialized():
             if ws == 1:
@@ -529,6 +532,11 @@ def run_ours(args, cfg):
                          "hbm_peak_gbs": hbm, "hbm_source": hbm_src,
                          "kernel_ms": kt},
             "cpu_baseline": cpu,
+            "determinism": ("AVS: the patch updates of a DoF are summed by fp64 bulk reduce-adds "
+                            "in arbitrary order (run-to-run differences ~1e-16 relative); "
+                            "DGB_AVS_ATOMIC=0 runs the deterministic colour order"
+                            if kind == "avs" and os.environ.get("DGB_AVS_ATOMIC", "1") != "0"
+                            else "deterministic launch order"),
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,

@@ -134,6 +134,17 @@ int dg_patch_fdm(const dg_level_t* lvl, const double* r, double* x,
 int dg_solve_range(const dg_level_t* lvl, int kind, double omega, const double* r,
                    double* x, int lo, int hi, void* stream);
 
+/* One colour of the multiplicative vertex-patch sweep restricted to the
+ * patches whose last vertex coordinate is in [vlo, vhi) (colour = index of
+ * the level's non-empty patch colours, sweep order): what & 1 computes the
+ * restricted residual r = b - A x on their cells, what & 2 the local solves
+ * x += omega A_j^-1 r_j (disjoint inside a colour).  The host wavefront
+ * pipeline of LevelSmoother (smooth_multiplicative on host vectors) chains
+ * these per z-chunk.  (LevelSmoother.smooth_multiplicative,
+ * smoothers.py:157-166)                                                    */
+int dg_mvs_range(const dg_level_t* lvl, int colour, int what, double omega, double* x,
+                 const double* b, double* r, int vlo, int vhi, void* stream);
+
 /* colour lists built at create time (device int32, owned by the level)     */
 int dg_num_colours(const dg_level_t* lvl, int kind);
 int dg_colour_list(const dg_level_t* lvl, int kind, int colour,
@@ -166,6 +177,9 @@ int dg_flow_enabled(const dg_level_t* lvl);
  * overlapped AVS DGB_AVS_WIN / DGB_AVS_OVERLAP, persistent solves DGB_FDM=5/6,
  * DMMA solves DGB_MMA), built only with -DDGB_EXPERIMENTAL.                 */
 #define DG_BUILD_EXPERIMENTAL 1
+/* DG_BUILD_CHECKS = device-side bounds checks of every cell address
+ * (-DDGB_CHECKS; a violation traps and the launch fails).                  */
+#define DG_BUILD_CHECKS 2
 int dg_build_flags(void);
 
 

@@ -78,5 +78,9 @@ class Staged:
             # a read-only array raises as numpy's in-place update would
             if not self.host.flags.writeable:
                 raise ValueError("assignment destination is read-only")
+            if self.host.flags.c_contiguous and self.host.dtype == np.float64:
+                # straight into the caller's memory (no temporary host vector)
+                torch.from_numpy(self.host.reshape(-1)).copy_(self.dev)
+                return
             out = self.dev.cpu().numpy()
             np.copyto(self.host, out.reshape(self.host.shape))

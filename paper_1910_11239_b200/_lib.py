@@ -30,7 +30,7 @@ EXPORTS = (
     "dg_patch_gather_map", "dg_smooth", "dg_last_launch_count", "dg_flow_enabled",
     "dg_build_flags",
     "dg_prolongate", "dg_restrict", "dg_cg_update", "dg_xpby", "dg_dot", "dg_solve_range",
-    "dg_dist_apply", "dg_dist_cell_fdm",
+    "dg_mvs_range", "dg_dist_apply", "dg_dist_cell_fdm",
 )
 
 
@@ -98,6 +98,7 @@ def load() -> ctypes.CDLL:
         "dg_xpby": ([vp, c_double, vp, i64, vp], c_int),
         "dg_dot": ([vp, vp, i64, vp, vp, vp], c_int),
         "dg_solve_range": ([vp, c_int, c_double, vp, vp, c_int, c_int, vp], c_int),
+        "dg_mvs_range": ([vp, c_int, c_int, c_double, vp, vp, vp, c_int, c_int, vp], c_int),
         "dg_dist_apply": ([vp, vp, vp, vp, vp], c_int),
         "dg_dist_cell_fdm": ([c_int, c_int, i64, vp, vp, vp, vp, c_double, vp, i64, vp], c_int),
     }

@@ -9,6 +9,7 @@
 //  - boundary digit per direction: bit 0 = left face on the boundary,
 //    bit 1 = right face (fastdiag.py:349-369, 535-566).
 #pragma once
+#include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -115,9 +116,31 @@ __device__ __forceinline__ void cell_multi(const Geo& g, int cell, int* c) {
   }
 }
 
+// DGB_CHECKS builds (__graft_entry__.build with DGB_CHECKS=1, the in-repo
+// stand-in for compute-sanitizer, which this GPU pool does not allow): every
+// cell a kernel addresses through cell_local is checked against the stored
+// window; a violation prints the site and traps (the launch then fails)
+#ifdef DGB_CHECKS
+#define DG_DEVICE_CHECK(cond, msg)                                                  \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("DGB_CHECKS: %s (%s:%d) block %d thread %d\n", msg, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                    \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define DG_DEVICE_CHECK(cond, msg) \
+  do {                             \
+  } while (0)
+#endif
+
 // global multi-index -> local cell id
 template <int D>
 __device__ __forceinline__ int cell_local(const Geo& g, const int* c) {
+  DG_DEVICE_CHECK(c[0] >= 0 && c[0] < g.nc[0] && (D == 2 || (c[1] >= 0 && c[1] < g.nc[1])) &&
+                      c[D - 1] >= g.zb && c[D - 1] < g.zb + g.zn,
+                  "cell outside the stored window");
   if (D == 2) return c[0] + g.nc[0] * (c[1] - g.zb);
   return c[0] + g.nc[0] * (c[1] + g.nc[1] * (c[2] - g.zb));
 }

@@ -113,6 +113,9 @@ struct dg_level {
   std::vector<DevList> pcol_pk;     // same, packed vertex coordinates
   std::vector<DevList> pcol_cells;  // cells covered by a patch colour (MVS), local ids
   std::vector<DevList> pcol_cells_pk;
+  // per colour of pcol_pk: voff[v] = entries with last vertex coordinate < v
+  // (the lists are in patch-id order, so a v_last range is a sub-list)
+  std::vector<std::vector<int64_t>> pcol_voff;
   std::vector<DevList> clus_pk;     // AVS clusters per cluster colour, packed base vertices
   DevList pall_pk;                  // all patches (colour order), packed, one-launch AVS
   std::vector<DevList> pwin_pk;     // AVS launch order: (z-window, parity class), packed
@@ -636,6 +639,16 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
       L->pcol_cells.push_back(b);
       if (!rc) rc = upload_list(pcp[k], &ap);
       L->pcol_pk.push_back(ap);
+      {
+        const int nv = nc[d - 1] + 1;
+        std::vector<int64_t> off(nv + 1, 0);
+        for (int32_t e : pcp[k]) {
+          const int vl = (d == 3) ? (e >> 20) & 1023 : (e >> 15) & 32767;
+          ++off[vl + 1];
+        }
+        for (int v = 1; v <= nv; ++v) off[v] += off[v - 1];
+        L->pcol_voff.push_back(off);
+      }
       if (!rc) rc = upload_list(ccp[k], &bp);
       L->pcol_cells_pk.push_back(bp);
       if (rc) { free_level(L); return rc; }
@@ -1059,6 +1072,31 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
   return fail(DG_EINVAL, "unknown smoother kind");
 }
 
+int dg_mvs_range(const dg_level_t* Lc, int colour, int what, double omega, double* x,
+                 const double* b, double* r, int vlo, int vhi, void* stream) {
+  dg_level_t* L = const_cast<dg_level_t*>(Lc);
+  if (!L || !x || !b || !r) return fail(DG_EINVAL, "null argument");
+  if (r == x || r == b) return fail(DG_EINVAL, "scratch residual must not alias x or b");
+  if (!L->has_patch) return fail(DG_EUNSUPPORTED, "vertex patches unsupported here");
+  if (colour < 0 || colour >= (int)L->pcol_pk.size()) return fail(DG_EINVAL, "colour out of range");
+  if (int rc = check_align(L, x, b, r)) return rc;
+  const auto& off = L->pcol_voff[colour];
+  const int nv = (int)off.size() - 1;
+  const int64_t i0 = off[std::min(std::max(vlo, 0), nv)], i1 = off[std::min(std::max(vhi, 0), nv)];
+  if (i1 <= i0) return DG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int cells = 1 << L->d;
+  if (what & 1) {
+    DevList l{L->pcol_cells_pk[colour].ptr + cells * i0, cells * (i1 - i0)};
+    if (int rc = res_packed(L, x, b, r, l, st, 1)) return rc;
+  }
+  if (what & 2) {
+    DevList l{L->pcol_pk[colour].ptr + i0, i1 - i0};
+    if (int rc = patch_fdm_packed(L, r, x, omega, l, st)) return rc;
+  }
+  return DG_OK;
+}
+
 int dg_smooth(dg_level_t* L, int kind, double omega, int reverse, double* x, const double* b,
               double* r, int use_graph, void* stream) {
   if (!L || !x || !b || !r) return fail(DG_EINVAL, "null argument");
@@ -1105,11 +1143,14 @@ int dg_flow_enabled(const dg_level_t* L) {
 }
 
 int dg_build_flags(void) {
+  int f = 0;
 #ifdef DGB_EXPERIMENTAL
-  return DG_BUILD_EXPERIMENTAL;
-#else
-  return 0;
+  f |= DG_BUILD_EXPERIMENTAL;
 #endif
+#ifdef DGB_CHECKS
+  f |= DG_BUILD_CHECKS;
+#endif
+  return f;
 }
 
 }  // extern "C"

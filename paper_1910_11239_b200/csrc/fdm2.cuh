@@ -538,7 +538,7 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
     for (int s = 0; s < R::SLOTS; ++s) {
       int c[3] = {base[0] + (s & 1), base[1] + ((s >> 1) & 1), base[2] + ((s >> 2) & 1)};
       if (!PATCH) c[0] = base[0], c[1] = base[1], c[2] = base[2];
-      s_cell[tid][s] = (int64_t)cell_local<D>(p.geo, c) * NEc;
+      s_cell[tid][s] = inf[7] ? (int64_t)cell_local<D>(p.geo, c) * NEc : 0;
     }
   }
   __syncthreads();

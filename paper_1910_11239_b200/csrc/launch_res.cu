@@ -2,6 +2,9 @@
 #include "launch.h"
 #include "res2.cuh"
 #include "res3.cuh"
+#ifdef DGB_EXPERIMENTAL
+#include "res4.cuh"
+#endif
 
 #include <algorithm>
 #include <cstring>
@@ -67,6 +70,29 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
       return DG_OK;
     }
   }
+#ifdef DGB_EXPERIMENTAL
+  if constexpr (D == 3 && N <= 6) {
+    // whole layers: slice-register passes on z-column segments (res4.cuh);
+    // measured slower at cfg 5 (0.91 vs 0.66 ms: 12 warps per SM and
+    // uncoalesced per-thread slice loads, profiles/r02): opt-in
+    const int64_t lc = (int64_t)q.geo.nc[0] * q.geo.nc[1];
+    if (!q.list && q.start % lc == 0 && q.count % lc == 0 && env_int("DGB_RES4", 0)) {
+      using S4 = Res4Shape<N>;
+      const int zl0 = (int)(q.start / lc), nzl = (int)(q.count / lc);
+      const int nseg = (nzl + S4::ZC - 1) / S4::ZC;
+      const size_t smem4 = sizeof(double) * S4::SMEM;
+      auto k4 = res4_kernel<N>;
+      static bool attr4 = false;
+      if (!attr4) {
+        DG_CUDA(cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4));
+        attr4 = true;
+      }
+      k4<<<(unsigned)(lc * nseg), S4::NT, smem4, st>>>(p, zl0, nzl);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
+  }
+#endif
   int64_t ngroups = (q.count + G - 1) / G;
   p.blocked = 0;
   p.bz0 = p.bnz = 0;

@@ -3,6 +3,7 @@ against the reference's golden vectors and the pinned CPU oracle.
 
 Tolerance (north star): relative L2 <= 1e-12 in fp64; index maps bit-exact.
 """
+import os
 import numpy as np
 import pytest
 import torch
@@ -563,3 +564,37 @@ def test_numpy_views_update_in_place_and_readonly_raises():
     ro.flags.writeable = False
     with pytest.raises(ValueError):
         sm.smooth(ro, b)
+
+
+def test_library_build_flags():
+    """The default library has neither the experimental variants nor the
+    bounds checks compiled in; a DGB_LIB build reports what it carries."""
+    from paper_1910_11239_b200 import _lib
+    flags = _lib.load().dg_build_flags()
+    if os.environ.get("DGB_LIB"):
+        assert flags >= 0
+    else:
+        assert flags == 0
+
+
+@pytest.mark.parametrize("k,nc,rev", [(3, 16, False), (7, 16, True), (2, 17, False)])
+def test_mvs_host_wavefront_pipeline_bitwise(k, nc, rev, monkeypatch):
+    """Host vectors take the wavefront-pipelined MVS sweep (dg_mvs_range per
+    colour and z-chunk, copies overlapped): bitwise the device sweep, for
+    numpy (eager) and pinned tensors (one CUDA graph), forward and reverse."""
+    monkeypatch.setenv("DGB_MVS_PIPELINE", "1")
+    ctx, _, sm = _setup(3, nc, k, "mvs", 1.0)
+    x0, b = inputs(ctx.ndofs, 17)
+    assert sm._mvs_pipelinable(x0, b)
+    xd = torch.from_numpy(x0).cuda()
+    sm.smooth(xd, torch.from_numpy(b).cuda(), reverse=rev)
+    want = xd.cpu().numpy()
+    xn = x0.copy()
+    sm.smooth(xn, b, reverse=rev)
+    assert np.array_equal(xn, want)
+    xh = torch.from_numpy(x0.copy()).pin_memory()
+    bh = torch.from_numpy(b).pin_memory()
+    for _ in range(2):  # capture, then replay
+        xh.copy_(torch.from_numpy(x0))
+        sm.smooth(xh, bh, reverse=rev)
+        assert np.array_equal(xh.numpy(), want)
