@@ -98,6 +98,7 @@ struct dg_level {
   const double *cz = nullptr, *czt = nullptr, *cinv = nullptr;
   const double *pz = nullptr, *pzt = nullptr, *pinv = nullptr;
   const double *ceod = nullptr, *peod = nullptr;  // device even/odd tables (tensor-core solves)
+  int* wcount = nullptr;  // work counter of the persistent solve kernel (fdm2p.cuh)
   double alpha = 0, beta = 0, betap = 0;
   bool has_patch = false;
   std::vector<double> hcz, hczt, hpz, hpzt;  // host copies for the kernel parameter space
@@ -147,6 +148,7 @@ static void free_level(dg_level* L) {
     for (auto& l : *v) cudaFree(l.ptr);
   cudaFree(L->pall_pk.ptr);
   cudaFree(L->dtab);
+  cudaFree(L->wcount);
   cudaFree(L->flow.tasks);
   cudaFree(L->flow.succ);
   cudaFree(L->flow.plist);
@@ -179,6 +181,7 @@ static FdmArgs fdm_params(const dg_level* L, bool patch, const double* r, double
   p.zd = patch ? L->pz : L->cz;
   p.ztd = patch ? L->pzt : L->czt;
   p.eod = patch ? L->peod : L->ceod;
+  p.counter = L->wcount;
   p.omega = omega;
   p.geo = L->geo;
   return p;
@@ -506,6 +509,11 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     L->pinv = dptr[8];
   }
   if (!L->hceo.empty()) L->ceod = dptr[ceo_at];
+  e = cudaMalloc(&L->wcount, 16 * sizeof(int));
+  if (e != cudaSuccess) {
+    free_level(L);
+    return fail(DG_ECUDA, std::string("cudaMalloc counter: ") + cudaGetErrorString(e));
+  }
   if (!L->hpeo.empty()) L->peod = dptr[peo_at];
 
   // ---- colour lists -------------------------------------------------------

@@ -50,6 +50,7 @@ struct FdmArgs {
   const double* zd = nullptr;   // device Z per digit (row-major m x m), tensor-core path
   const double* ztd = nullptr;  // device Z^T per digit
   const double* eod = nullptr;  // device even/odd halves of the interior digit (4 tables)
+  int* counter = nullptr;       // device work counter of the persistent solve (fdm2p.cuh)
   double omega = 0;
   Geo geo;
 };

@@ -4,6 +4,9 @@
 #include "launch.h"
 #include "fdm2.cuh"
 #ifdef DGB_EXPERIMENTAL
+#include "fdm2p.cuh"
+#endif
+#ifdef DGB_EXPERIMENTAL
 #include "fdm4.cuh"
 #endif
 #ifdef DGB_EXPERIMENTAL
@@ -147,6 +150,30 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
         const int resident3v = resident3[v3 & 1];
         const int64_t ng3 = (q.count + S3::G - 1) / S3::G;
         k3<<<(unsigned)std::min<int64_t>(ng3, resident3v), S3::NT, smem3, st>>>(p, ng3);
+        DG_CUDA(cudaGetLastError());
+        return DG_OK;
+      }
+    }
+#endif
+#ifdef DGB_EXPERIMENTAL
+    // persistent, with the next group's cells prefetched (fdm2p.cuh): measured
+    // 2x slower at cfg 5 (3.9 vs 1.8 ms: spills at 3 CTAs/SM, the digit
+    // switch compiled to register-indexed constant loads, doubled x write-back)
+    if constexpr (Rows<D, M, PATCH>::N % 8 != 0) {
+      const int vp = env_int("DGB_FDM2P", 0);
+      if (p.direct == 2 && !q.cluster && q.counter && vp) {
+        using SP = Fdm2pShape<D, M, PATCH>;
+        auto kp = vp == 2 ? fdm2p_kernel<D, M, PATCH, 2> : fdm2p_kernel<D, M, PATCH, 3>;
+        const size_t smemp = sizeof(double) * SP::SMEM;
+        static int residentp_[2] = {0, 0};
+        int& residentp = residentp_[vp == 2];
+        if (!residentp) {
+          DG_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemp));
+          if (int rc = resident_ctas(kp, SP::NT, smemp, &residentp)) return rc;
+        }
+        const int64_t ngp = (q.count + SP::G - 1) / SP::G;
+        DG_CUDA(cudaMemsetAsync(q.counter, 0, sizeof(int), st));
+        kp<<<(unsigned)std::min<int64_t>(ngp, residentp), SP::NT, smemp, st>>>(p, ngp, q.counter);
         DG_CUDA(cudaGetLastError());
         return DG_OK;
       }
