@@ -504,8 +504,47 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
   constexpr int NT = G * F;
   __shared__ int s_info[G][8];            // digit[3], cls, active
   __shared__ int64_t s_cell[G][R::SLOTS];  // dof offset of each cell of the subdomain
+  __shared__ __align__(8) uint64_t s_bar;
   const int tid = threadIdx.x;
-  if (tid < G) {
+  if constexpr (BULK) {
+    // prologue of the bulk path: the lanes of warp 0 take one (subdomain,
+    // cell) each, compute its offset and issue its copy at once; one CTA
+    // barrier.  (ncu r02, cfg 5: a quarter of the stall samples sat in the
+    // old prologue -- subdomain info by G threads, a barrier, the copies, a
+    // second barrier -- before the copies' own latency.)
+    if (tid < 32) {
+      if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        const int64_t left = count - grp * G;
+        const int nact = left < G ? (int)left : G;
+        mbar_expect_tx(&s_bar, (unsigned)(nact * R::SLOTS * NEc * 8));
+      }
+      __syncwarp();
+      for (int l = tid; l < G * R::SLOTS; l += 32) {
+        const int gg = l / R::SLOTS, sl = l - gg * R::SLOTS;
+        const int64_t idx = grp * G + gg;
+        const bool act = idx < count;
+        int digit[3] = {0, 0, 0}, base[3] = {0, 0, 0};
+        if (act) subdomain_info<D, PATCH>(p.geo, list ? list[idx] : (int)(start + idx), packed != 0,
+                                          digit, base);
+        if (sl == 0) {
+          int* inf = s_info[gg];
+          int cls = 0;
+#pragma unroll
+          for (int t = D - 1; t >= 0; --t) cls = cls * 4 + digit[t];
+#pragma unroll
+          for (int t = 0; t < 3; ++t) inf[t] = digit[t];
+          inf[6] = cls;
+          inf[7] = act;
+        }
+        int c[3] = {base[0] + (sl & 1), base[1] + ((sl >> 1) & 1), base[2] + ((sl >> 2) & 1)};
+        if (!PATCH) c[0] = base[0], c[1] = base[1], c[2] = base[2];
+        const int64_t off = act ? (int64_t)cell_local<D>(p.geo, c) * NEc : 0;
+        s_cell[gg][sl] = off;
+        if (act) bulk_load(sm + gg * fdm_gstride<D, M, G>() + dense_off<NEc>(sl), p.r + off, NEc * 8, &s_bar);
+      }
+    }
+  } else if (tid < G) {
     const int64_t idx = grp * G + tid;
     int* inf = s_info[tid];
     inf[7] = idx < count;
@@ -555,27 +594,8 @@ __device__ __forceinline__ void fdm_group(const Fdm2Params<D, M>& p, const int32
   // reduce-add; the SM's load/store pipe only sees shared memory
   // (caller guarantees: NEc even, not coherent, not atomic, no cluster delta)
   static_assert(!BULK || dense_off<NEc>(R::SLOTS - 1) + NEc <= GSZ, "dense staging fits");
-  __shared__ __align__(8) uint64_t s_bar;
   if constexpr (BULK) {
-    // warp 0 issues the G * 2^d cell copies in parallel (one per lane); the
-    // single arrival (lane 0's expect_tx) keeps the phase open until all land
-    if (tid < 32) {
-      if (tid == 0) mbar_init(&s_bar, 1);
-      __syncwarp();
-      if (tid == 0) {
-        unsigned bytes = 0;
-        for (int gg = 0; gg < G; ++gg)
-          if (s_info[gg][7]) bytes += R::SLOTS * NEc * 8;
-        mbar_expect_tx(&s_bar, bytes);
-      }
-      for (int l = tid; l < G * R::SLOTS; l += 32) {
-        const int gg = l / R::SLOTS, sl = l - gg * R::SLOTS;
-        if (s_info[gg][7])
-          bulk_load(sm + gg * GSZ + dense_off<NEc>(sl), p.r + s_cell[gg][sl], NEc * 8, &s_bar);
-      }
-    }
-    __syncthreads();  // barrier initialised before anyone waits on it
-    mbar_wait(&s_bar, 0);
+    mbar_wait(&s_bar, 0);  // the copies issued in the prologue
     double v[M], o[M];
     if (active) {
 #pragma unroll

@@ -153,19 +153,19 @@ __device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, i
                                              const int* c, const double* X, double* out,
                                              const double* XR = nullptr,
                                              const double* XL = nullptr,
-                                             const FacePre* pre = nullptr) {
+                                             FacePre pre = FacePre{-1, 0.0, 0.0}) {
   using L = Lay<D, N>;
   const int sb = LY::sbase(t, f), ss = LY::sstride(t);
   const int digit = (c[t] == 0 ? 1 : 0) | (c[t] == p.geo.nc[t] - 1 ? 2 : 0);
   const int gb = L::gbase(t, f), gs = L::gstride(t);
   int nb[3] = {c[0], c[1], D == 3 ? c[2] : 0};
   double r_hi = 0.0, r_all = 0.0, l_lo = 0.0, l_all = 0.0;
-  if (pre && pre->side == 1) {
-    r_hi = pre->hi, r_all = pre->all;
-  } else if (pre && pre->side == 0) {
-    l_lo = pre->hi, l_all = pre->all;
+  if (pre.side == 1) {
+    r_hi = pre.hi, r_all = pre.all;
+  } else if (pre.side == 0) {
+    l_lo = pre.hi, l_all = pre.all;
   }
-  if (!(digit & 2) && !(pre && pre->side == 1)) {  // a_pm x_R: value and normal derivative at the shared face
+  if (!(digit & 2) && pre.side != 1) {  // a_pm x_R: value and normal derivative at the shared face
     double xr[N];
     if (XR) {  // neighbour tensor of the same CTA block (shared memory)
 #pragma unroll
@@ -186,7 +186,7 @@ __device__ __forceinline__ void stiff2_fiber(const Res2Params<D, N>& p, int t, i
     r_all = p.betap * xr[0];
     r_hi = p.alpha * xr[0] + p.beta * g;
   }
-  if (!(digit & 1) && !(pre && pre->side == 0)) {  // a_pm^T x_L
+  if (!(digit & 1) && pre.side != 0) {  // a_pm^T x_L
     double xl[N];
     if (XL) {
 #pragma unroll
@@ -291,31 +291,32 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
   using LY = RLay<D, N, G, NARROW>;
   constexpr int GS = LY::GS;
   constexpr int RPC = (D == 3) ? N * N : N;  // rows per cell
-  // blocked mode: every cell has one out-of-block face per direction (the
-  // side away from its block partner); its neighbour fiber comes from global
-  // memory.  Load those first and reduce them to their two face scalars, so
-  // their latency overlaps the block's row loads instead of stalling the
-  // contraction phases (ncu r02: long-scoreboard stalls 21%).
-  FacePre pre[D];
-  if constexpr (D == 3 && G == 8) {
-    if (blocked) {
-      const int g0 = tid / Lay<D, N>::F, f0 = tid - g0 * Lay<D, N>::F;
-      const int* cc = s_c[g0];
-#pragma unroll
-      for (int t = 0; t < D; ++t) {
-        const bool right = (g0 >> t) & 1;  // high cell of the pair: +e_t is outside
-        const bool at_bnd = right ? cc[t] == p.geo.nc[t] - 1 : cc[t] == 0;
-        pre[t].side = (s_cell[g0] < 0 || at_bnd) ? -1 : (right ? 1 : 0);
-        pre[t].hi = pre[t].all = 0.0;
-        if (pre[t].side >= 0) face_pair<D, N>(p, t, f0, cc, right, pre[t].hi, pre[t].all);
-      }
-    }
-  }
   for (int row = tid; row < G * RPC; row += NT) {
     const int gg = row / RPC, w = row - gg * RPC;
     const int cell = s_cell[gg];
     if (cell < 0) continue;
     row_load<N>(sm + gg * GS + LY::row(w), p.x + (int64_t)cell * L::NE + w * N);
+  }
+  // blocked mode: every cell has one out-of-block face per direction (the
+  // side away from its block partner), whose neighbour fiber comes from
+  // global memory; those loads are issued here, behind the block's row
+  // loads, so their latency overlaps the barrier instead of the phases
+  // (measured: cfg 2, n = 4, residual 0.042 -> 0.037 ms; n = 6 loses, 0.663 ->
+  // 0.693 ms at cfg 5, so it stays off there)
+  FacePre pre0{-1, 0.0, 0.0}, pre1{-1, 0.0, 0.0}, pre2{-1, 0.0, 0.0};
+  if constexpr (D == 3 && G == 8 && N <= 4) {
+    if (blocked) {
+      const int g0 = tid / Lay<D, N>::F, f0 = tid - g0 * Lay<D, N>::F;
+      const int* cc = s_c[g0];
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        FacePre& pr = t == 0 ? pre0 : (t == 1 ? pre1 : pre2);
+        const bool right = (g0 >> t) & 1;  // high cell of the pair: +e_t is outside
+        const bool at_bnd = right ? cc[t] == p.geo.nc[t] - 1 : cc[t] == 0;
+        pr.side = (s_cell[g0] < 0 || at_bnd) ? -1 : (right ? 1 : 0);
+        if (pr.side >= 0) face_pair<D, N>(p, t, f0, cc, right, pr.hi, pr.all);
+      }
+    }
   }
   // thread -> (cell, fiber) per direction
   int gt[3], ft[3];
@@ -335,13 +336,10 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
     return s_cell[gn] >= 0 ? sm + gn * GS : nullptr;
   };
   __syncthreads();
-  const bool usepre = D == 3 && G == 8 && blocked;
   if (act(0))
-    stiff2_fiber<D, N, LY>(p, 0, ft[0], s_c[gt[0]], X(0), A(0), nbr(0, true), nbr(0, false),
-                           usepre ? &pre[0] : nullptr);
+    stiff2_fiber<D, N, LY>(p, 0, ft[0], s_c[gt[0]], X(0), A(0), nbr(0, true), nbr(0, false), pre0);
   if (act(1))
-    stiff2_fiber<D, N, LY>(p, 1, ft[1], s_c[gt[1]], X(1), B(1), nbr(1, true), nbr(1, false),
-                           usepre ? &pre[D > 1 ? 1 : 0] : nullptr);
+    stiff2_fiber<D, N, LY>(p, 1, ft[1], s_c[gt[1]], X(1), B(1), nbr(1, true), nbr(1, false), pre1);
   __syncthreads();
   if (act(1)) mass_fiber<D, N, false, LY>(p, 1, ft[1], A(1), nullptr);
   if (act(0)) mass_fiber<D, N, false, LY>(p, 0, ft[0], B(0), nullptr);
@@ -356,7 +354,7 @@ __device__ __forceinline__ void res_group(const Res2Params<D, N>& p, const int32
     if (act(2)) {
       mass_fiber<D, N, true, LY>(p, 2, ft[2], A(2), B(2));  // A = M_2 (M_1 G_0 + M_0 G_1)
       stiff2_fiber<D, N, LY>(p, 2, ft[2], s_c[gt[2]], X(2), B(2), nbr(2, true),
-                             nbr(2, false), usepre ? &pre[D - 1] : nullptr);                 // B = G_2
+                             nbr(2, false), pre2);                 // B = G_2
     }
     __syncthreads();
     if (act(0) && p.b) row_load_reg<N>(bv, p.b + gi);
