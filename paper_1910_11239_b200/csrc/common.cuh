@@ -97,6 +97,9 @@ struct Lay {
 template <int D, int M>
 __host__ __device__ constexpr int fdm2_groups() {
   constexpr int F = Lay<D, M>::F;
+#ifdef FDM_G12
+  if (D == 3 && M == 12) return FDM_G12;
+#endif
   for (int g = 1; g <= 32; ++g)
     if ((g * F) % 32 == 0 && g * F >= 128 && g * F <= 512) return g;
   return F >= 128 ? 1 : (128 + F - 1) / F;
