@@ -28,6 +28,8 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
   p.beta = q.beta;
   p.betap = q.betap;
   p.geo = q.geo;
+  p.blocked = 0;
+  p.bz0 = p.bnz = 0;
   for (int i = 0; i < N; ++i)
     for (int k = 0; k < N; ++k) {
       p.mats.mass[k * N + i] = h.mass[i * N + k];
@@ -59,10 +61,45 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
       auto k3 = minb >= HI ? res3_kernel<N, HI>
                            : (minb >= MID ? res3_kernel<N, MID>
                                           : (minb >= 3 ? res3_kernel<N, 3> : res3_kernel<N, 2>));
+#ifdef DGB_EXPERIMENTAL
+      // batched trace phase (res3b_kernel): measured no faster, opt-in
+      if (env_int("DGB_RES3_BATCH", 0))
+        k3 = minb >= HI ? res3b_kernel<N, HI>
+                        : (minb >= MID ? res3b_kernel<N, MID>
+                                       : (minb >= 3 ? res3b_kernel<N, 3> : res3b_kernel<N, 2>));
+      if constexpr (N % 2 == 0) {
+        // direction-0 rows staged by TMA bulk copies (res3c_kernel, DGB_RES3_TMA)
+        if (env_int("DGB_RES3_TMA", 0)) {
+          using SC = Res3cShape<N>;
+          const size_t smemc = sizeof(double) * SC::SMEM;
+          auto kc = minb >= HI ? res3c_kernel<N, HI>
+                               : (minb >= MID ? res3c_kernel<N, MID>
+                                              : (minb >= 3 ? res3c_kernel<N, 3> : res3c_kernel<N, 2>));
+          static bool attrc = false;
+          if (!attrc) {
+            for (auto kk : {res3c_kernel<N, 2>, res3c_kernel<N, 3>, res3c_kernel<N, MID>,
+                            res3c_kernel<N, HI>})
+              DG_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smemc));
+            attrc = true;
+          }
+          p.blocked = (S::G == 2 && q.list && q.block_list && q.count % 8 == 0 &&
+                       env_int("DGB_RES_BLOCK_LIST", 1)) ? 2 : 0;
+          kc<<<grid, S::NT, smemc, st>>>(p);
+          DG_CUDA(cudaGetLastError());
+          return DG_OK;
+        }
+      }
+#endif
       static bool attr3 = false;
       if (!attr3) {
         for (auto kk : {res3_kernel<N, 2>, res3_kernel<N, 3>, res3_kernel<N, MID>, res3_kernel<N, HI>})
           DG_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+#ifdef DGB_EXPERIMENTAL
+        for (auto kk : {res3b_kernel<N, 2>, res3b_kernel<N, 3>, res3b_kernel<N, MID>,
+                        res3b_kernel<N, HI>})
+          DG_CUDA(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+#endif
         attr3 = true;
       }
       k3<<<grid, S::NT, smem3, st>>>(p);
