@@ -173,7 +173,7 @@ class DeviceLevel:
         t.cell_invsum = arr(dt.cell_invsum)
         t.cell_eo = arr(dt.cell_eo)
         t.res_eo = arr(dt.res_eo)
-        if dt.patch_z is not None and tables.n <= 8:
+        if dt.patch_z is not None:
             t.patch_z = arr(dt.patch_z)
             t.patch_zt = arr(np.transpose(dt.patch_z, (0, 2, 1)))
             t.patch_invsum = arr(dt.patch_invsum)

@@ -99,6 +99,8 @@ struct dg_level {
   const double *pz = nullptr, *pzt = nullptr, *pinv = nullptr;
   const double *ceod = nullptr, *peod = nullptr;  // device even/odd tables (tensor-core solves)
   int* wcount = nullptr;  // work counter of the persistent solve kernel (fdm2p.cuh)
+  double* big_scratch = nullptr;  // per-CTA patch tensors of the generic solve (fdmg.cuh)
+  int big_slots = 0;
   double alpha = 0, beta = 0, betap = 0;
   bool has_patch = false;
   std::vector<double> hcz, hczt, hpz, hpzt;  // host copies for the kernel parameter space
@@ -149,6 +151,7 @@ static void free_level(dg_level* L) {
   cudaFree(L->pall_pk.ptr);
   cudaFree(L->dtab);
   cudaFree(L->wcount);
+  cudaFree(L->big_scratch);
   cudaFree(L->flow.tasks);
   cudaFree(L->flow.succ);
   cudaFree(L->flow.plist);
@@ -182,6 +185,10 @@ static FdmArgs fdm_params(const dg_level* L, bool patch, const double* r, double
   p.ztd = patch ? L->pzt : L->czt;
   p.eod = patch ? L->peod : L->ceod;
   p.counter = L->wcount;
+  if (patch) {
+    p.big_scratch = L->big_scratch;
+    p.big_slots = L->big_slots;
+  }
   p.omega = omega;
   p.geo = L->geo;
   return p;
@@ -447,7 +454,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   L->alpha = T->alpha;
   L->beta = T->beta;
   L->betap = T->betap;
-  L->has_patch = T->patch_z != nullptr && n <= 8;
+  L->has_patch = T->patch_z != nullptr;
   L->hmass.assign(T->mass, T->mass + n * n);
   L->hadiag.assign(T->adiag, T->adiag + 4 * n * n);
   L->hbg.assign(T->bg, T->bg + 2 * n);
@@ -515,6 +522,22 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     return fail(DG_ECUDA, std::string("cudaMalloc counter: ") + cudaGetErrorString(e));
   }
   if (!L->hpeo.empty()) L->peod = dptr[peo_at];
+  if (L->has_patch) {
+    // degree >= 8 patches run the generic kernel; its 3D m = 32 tensor does
+    // not fit in shared memory and lives in a per-CTA slice of this buffer
+    const size_t sb = patch_fdm_scratch_bytes(d, n);
+    if (sb) {
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      L->big_slots = 2 * std::max(1, sms);
+      e = cudaMalloc(&L->big_scratch, sb * (size_t)L->big_slots);
+      if (e != cudaSuccess) {
+        free_level(L);
+        return fail(DG_ECUDA, std::string("cudaMalloc patch scratch: ") + cudaGetErrorString(e));
+      }
+    }
+  }
 
   // ---- colour lists -------------------------------------------------------
   const int* nc = desc->ncells;

@@ -51,6 +51,8 @@ struct FdmArgs {
   const double* ztd = nullptr;  // device Z^T per digit
   const double* eod = nullptr;  // device even/odd halves of the interior digit (4 tables)
   int* counter = nullptr;       // device work counter of the persistent solve (fdm2p.cuh)
+  double* big_scratch = nullptr;  // per-CTA tensors of the generic kernel (fdmg.cuh), or null
+  int big_slots = 0;              // tensors big_scratch holds
   double omega = 0;
   Geo geo;
 };
@@ -102,6 +104,7 @@ int dispatch_cell_fdm(int d, int n, const FdmArgs& p, const double* hz, const do
                       const double* heo, cudaStream_t st);
 int dispatch_patch_fdm(int d, int n, const FdmArgs& p, const double* hz, const double* hzt,
                        const double* heo, cudaStream_t st);
+size_t patch_fdm_scratch_bytes(int d, int n);
 bool flow_shape(int d, int n, int* gp, int* gr);
 int dispatch_flow(int d, int n, const ResArgs& ra, const FdmArgs& fa, const HostRes& h,
                   const double* hz, const double* hzt, const double* heo, const FlowDev& fd,

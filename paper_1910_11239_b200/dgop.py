@@ -152,7 +152,7 @@ def make_context(level, basis, gamma_hat: float = 1.0,
     h = _level_h(level)
     layout = DofLayout(dim=len(dims), degree=b.degree, dims=tuple(dims))
     tables = build_tables(b, h, tuple(dims), gamma_hat,
-                          with_patches=b.n <= 8 and min(dims) >= 2)
+                          with_patches=min(dims) >= 2)
     return OperatorContext(level, b, layout, gamma_hat, tables, counter)
 
 

@@ -262,7 +262,7 @@ class PatchSolverSet(_SolverSetBase):
         self.patch_dofs = self.m1 ** self.dim
         self.cell_dofs = self.basis.n ** self.dim
         if self.ctx.tables.patch_z is None and len(self.patches):
-            raise NotImplementedError("vertex patches on the device support degree <= 7")
+            raise NotImplementedError("vertex patches need at least 2 cells per direction")
         v = self.patches.vertex_indices
         self._build_classes(_class_codes(v, np.array(dims) - 1, 1) if len(v)
                             else np.zeros(0, dtype=np.int64))

@@ -79,3 +79,15 @@ def ref_dgmg():
                 sys.path.insert(0, path)
             return importlib.import_module("dgmg")
     return None
+
+
+GOLDEN_BIG = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_big.npz")
+_gold_big = None
+
+
+def golden_big():
+    """Degree 8..15 vertex-patch steps and 1D levels (tests/golden/make_golden_big.py)."""
+    global _gold_big
+    if _gold_big is None:
+        _gold_big = dict(np.load(GOLDEN_BIG))
+    return _gold_big

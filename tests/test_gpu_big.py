@@ -1,0 +1,110 @@
+"""GPU parity beyond the templated kernels: vertex patches of degree 8..15
+(generic kernel csrc/fdmg.cuh: patch tensors of 18..32 per direction, the
+3D m = 32 tensor in a global scratch slice) against the reference's golden
+steps (tests/golden/make_golden_big.py) and the pinned oracle.
+
+Tolerance (north star): relative L2 <= 1e-12 in fp64; index maps bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+from _common import golden_big, inputs, rel, RTOL
+
+import paper_1910_11239_b200 as dg
+from paper_1910_11239_b200 import fastdiag as fd
+from oracle.sipg_oracle import OracleLevel
+
+pytestmark = pytest.mark.gpu
+G = golden_big()
+STEPS = sorted({k.split("/")[0] for k in G if k.startswith("sm_") and "_1d_" not in k})
+OPS = sorted({k.split("/")[0] for k in G if k.startswith("op_") and "_1d_" not in k})
+
+
+def _setup(d, nc, k, kind="acs", omega=1.0):
+    lvl = dg.build_hierarchy(d, nc, 0).levels[0]
+    basis = dg.Basis1D.make(k)
+    ctx = dg.make_context(lvl, basis, 1.0)
+    sm = dg.make_level_smoother(ctx, basis, dg.SmootherConfig(kind=kind, omega=omega))
+    return ctx, basis, sm
+
+
+@pytest.mark.parametrize("name", STEPS)
+def test_step_matches_reference(name):
+    kind = name.split("_")[1]
+    d, nc, k, om, rev = G[name + "/meta"]
+    ctx, _, sm = _setup(int(d), int(nc), int(k), kind, float(om))
+    x0, b = inputs(ctx.ndofs)
+    x = x0.copy()
+    sm.smooth(x, b, reverse=bool(rev))
+    assert rel(x, G[name + "/x"]) <= RTOL
+    assert rel(x - x0, G[name + "/x"] - x0) <= 1e-11
+
+
+@pytest.mark.parametrize("name", OPS)
+def test_operator_matches_reference(name):
+    _, d, k, nc = name.split("_")
+    d, k, nc = int(d[0]), int(k[1:]), int(nc[1:])
+    ctx, _, _ = _setup(d, nc, k)
+    x0, b = inputs(ctx.ndofs)
+    assert rel(dg.apply_operator(ctx, x0), G[name + "/Ax"]) <= RTOL
+    assert rel(dg.residual(ctx, x0, b, out=np.empty(ctx.ndofs)), G[name + "/res"]) <= RTOL
+
+
+@pytest.mark.parametrize("kind,d,nc,k,omega", [
+    ("avs", 3, 4, 8, 0.25),    # m = 18, 27 patches, all boundary classes + interior
+    ("mvs", 3, 4, 10, 1.0),    # m = 22
+    ("avs", 3, 3, 13, 0.125),  # m = 28 (shared memory, padded pitch)
+    ("mvs", 3, 3, 14, 1.0),    # m = 30 (shared memory, the largest that fits)
+    ("avs", 3, 4, 15, 0.25),   # m = 32 (global scratch), 27 patches
+    ("mvs", 2, 9, 13, 1.0),    # 2D m = 28
+    ("avs", 2, 7, 15, 0.25),   # 2D m = 32
+])
+def test_step_matches_oracle(kind, d, nc, k, omega):
+    ctx, _, sm = _setup(d, nc, k, kind, omega)
+    x0, b = inputs(ctx.ndofs, 3)
+    x = torch.from_numpy(x0).cuda()
+    sm.smooth(x, torch.from_numpy(b).cuda())
+    want = OracleLevel((nc,) * d, k).smooth(kind, omega, x0, b)
+    got = x.cpu().numpy()
+    assert rel(got, want) <= RTOL
+    assert rel(got - x0, want - x0) <= 1e-11
+
+
+@pytest.mark.parametrize("d,nc,k", [(3, 3, 9), (2, 5, 12), (3, 2, 15)])
+def test_gather_maps_bit_exact_big(d, nc, k):
+    lvl = dg.build_hierarchy(d, nc, 0).levels[0]
+    pset = fd.PatchSolverSet(lvl, dg.Basis1D.make(k), 1.0)
+    o = OracleLevel((nc,) * d, k)
+    want = o.patch_map(o.patch_vertices())
+    got = pset.gather_map(np.arange(len(pset.patches)))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("d,nc,k", [(3, 3, 8), (2, 6, 11)])
+def test_patch_solver_set_safe_accumulate_big(d, nc, k):
+    """All patches at once with overlap-safe accumulation, and a write-disjoint
+    colour, against the oracle (`fastdiag.py:602-628`)."""
+    lvl = dg.build_hierarchy(d, nc, 0).levels[0]
+    pset = fd.PatchSolverSet(lvl, dg.Basis1D.make(k), 1.0)
+    o = OracleLevel((nc,) * d, k)
+    _, r = inputs(o.ndofs, 7)
+    x = np.zeros(o.ndofs)
+    pset.solve_scaled_into(x, r, None, 0.5, safe_accumulate=True)
+    want = np.zeros(o.ndofs)
+    o.patch_solve(want, r, 0.5, safe=True)
+    assert rel(x, want) <= RTOL
+
+
+@pytest.mark.parametrize("d,nc,k", [(3, 2, 8), (2, 4, 11)])
+def test_single_big_patch_solve_is_exact(d, nc, k):
+    """R_j A R_j^T y = R_j r for one patch (dense restriction of the oracle's matrix)."""
+    lvl = dg.build_hierarchy(d, nc, 0).levels[0]
+    pset = fd.PatchSolverSet(lvl, dg.Basis1D.make(k), 1.0)
+    o = OracleLevel((nc,) * d, k)
+    _, r = inputs(o.ndofs, 7)
+    a = o.dense()
+    gi = pset.subdomain_indices(0)
+    y = np.zeros(o.ndofs)
+    pset.solve_scaled_into(y, r, np.array([0]), 1.0)
+    assert rel(a[np.ix_(gi, gi)] @ y[gi], r[gi]) <= 1e-10

@@ -324,12 +324,14 @@ def _read_i32(ptr, cnt):
     return torch.as_tensor(_View(), device="cuda").cpu().numpy().copy()
 
 
-def test_unsupported_patch_degree_raises():
+def test_patch_degree_above_templates_is_supported():
+    """Degree 8 patches (m = 18) run the generic kernel (csrc/fdmg.cuh); the
+    reference has no degree limit (`fastdiag.py:510-634`)."""
     lvl = dg.build_hierarchy(3, 3, 0).levels[0]
     basis = dg.Basis1D.make(8)
     ctx = dg.make_context(lvl, basis)
-    with pytest.raises(NotImplementedError):
-        dg.make_level_smoother(ctx, basis, dg.SmootherConfig("avs", 0.25))
+    sm = dg.make_level_smoother(ctx, basis, dg.SmootherConfig("avs", 0.25))
+    assert sm.solvers.m1 == 18
 
 
 @experimental
