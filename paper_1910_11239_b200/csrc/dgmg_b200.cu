@@ -36,9 +36,9 @@ int fail(int code, const std::string& msg) {
 
 
 __global__ void gather_map_kernel(MapParams p) {
-  const int64_t per = (p.d == 3) ? (int64_t)p.m * p.m * p.m : (int64_t)p.m * p.m;
+  const int64_t per = (p.d == 3) ? (int64_t)p.m * p.m * p.m : (p.d == 2 ? (int64_t)p.m * p.m : p.m);
   const int64_t total = p.count * per;
-  const int NEc = (p.d == 3) ? p.n * p.n * p.n : p.n * p.n;
+  const int NEc = (p.d == 3) ? p.n * p.n * p.n : (p.d == 2 ? p.n * p.n : p.n);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = t / per;
@@ -55,7 +55,8 @@ __global__ void gather_map_kernel(MapParams p) {
       mul *= p.n;
     }
     int64_t cell;
-    if (p.d == 2) cell = c[0] + (int64_t)p.geo.nc[0] * (c[1] - p.geo.zb);
+    if (p.d == 1) cell = c[0] - p.geo.zb;
+    else if (p.d == 2) cell = c[0] + (int64_t)p.geo.nc[0] * (c[1] - p.geo.zb);
     else cell = c[0] + (int64_t)p.geo.nc[0] * (c[1] + (int64_t)p.geo.nc[1] * (c[2] - p.geo.zb));
     p.out[t] = cell * NEc + off;
   }
@@ -171,6 +172,8 @@ static ResArgs res_params(const dg_level* L, const double* x, const double* b, d
   p.alpha = L->alpha;
   p.beta = L->beta;
   p.betap = L->betap;
+  p.oned.adiag = L->adiag;
+  p.oned.bg = L->bg;
   p.geo = L->geo;
   return p;
 }
@@ -411,7 +414,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   if (!desc || !T || !out) return fail(DG_EINVAL, "null argument");
   *out = nullptr;
   const int d = desc->dim;
-  if (d != 2 && d != 3) return fail(DG_EUNSUPPORTED, "device path supports dim 2 and 3");
+  if (d < 1 || d > 3) return fail(DG_EUNSUPPORTED, "device path supports dim 1, 2 and 3");
   const int n = desc->degree + 1;
   if (desc->degree < 1 || n > 16)
     return fail(DG_EUNSUPPORTED, "device path supports 1 <= degree <= 15");
@@ -438,9 +441,10 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   L->d = d;
   L->n = n;
   L->m = 2 * n;
-  L->layer_cells = (d == 3) ? (int64_t)desc->ncells[0] * desc->ncells[1] : desc->ncells[0];
+  L->layer_cells = (d == 3) ? (int64_t)desc->ncells[0] * desc->ncells[1]
+                            : (d == 2 ? desc->ncells[0] : 1);
   L->ncells_local = L->layer_cells * desc->z_count;
-  L->cell_dofs = (d == 3) ? (int64_t)n * n * n : (int64_t)n * n;
+  L->cell_dofs = (d == 3) ? (int64_t)n * n * n : (d == 2 ? (int64_t)n * n : n);
   L->ndofs = L->ncells_local * L->cell_dofs;
   L->geo.nc[0] = desc->ncells[0];
   L->geo.nc[1] = d >= 2 ? desc->ncells[1] : 1;
@@ -468,8 +472,9 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
     if (T->patch_eo) L->hpeo.assign(T->patch_eo, T->patch_eo + 4 * n * n);
   }
   const int m = L->m;
-  const int64_t pw = (d == 3) ? 64 : 16;  // 4^d classes
-  const int64_t ce = L->cell_dofs, pe = (d == 3) ? (int64_t)m * m * m : (int64_t)m * m;
+  const int64_t pw = (d == 3) ? 64 : (d == 2 ? 16 : 4);  // 4^d classes
+  const int64_t ce = L->cell_dofs,
+                pe = (d == 3) ? (int64_t)m * m * m : (d == 2 ? (int64_t)m * m : m);
   std::vector<std::pair<const double*, int64_t>> parts = {
       {T->mass, n * n},  {T->adiag, 4 * n * n}, {T->bg, 2 * n},
       {T->cell_z, 4 * n * n}, {T->cell_zt, 4 * n * n}, {T->cell_invsum, pw * ce}};
@@ -543,6 +548,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   const int* nc = desc->ncells;
   const int zb = desc->z_begin;
   auto local_of = [&](const int* c) -> int32_t {
+    if (d == 1) return (int32_t)(c[0] - zb);
     if (d == 2) return (int32_t)(c[0] + (int64_t)nc[0] * (c[1] - zb));
     return (int32_t)(c[0] + (int64_t)nc[0] * (c[1] + (int64_t)nc[1] * (c[2] - zb)));
   };
@@ -602,7 +608,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
         }
         const int col = parq * 2 + (half & 1);
         pc[col].push_back((int32_t)id);
-        pcp[col].push_back(pack_d(d, v[0], v[1], d == 3 ? v[2] : 0));
+        pcp[col].push_back(pack_d(d, v[0], d >= 2 ? v[1] : 0, d == 3 ? v[2] : 0));
         for (int s = 0; s < (1 << d); ++s) {
           int c[3] = {0, 0, 0};
           for (int t = 0; t < d; ++t) c[t] = v[t] - 1 + ((s >> t) & 1);
@@ -651,7 +657,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
           std::vector<int32_t> lst;
           for (int k = 2 * q; k <= 2 * q + 1; ++k)
             for (int32_t e : pcp[k]) {
-              const int vl = (d == 3) ? (e >> 20) & 1023 : (e >> 15) & 32767;
+              const int vl = (d == 3) ? (e >> 20) & 1023 : (d == 2 ? (e >> 15) & 32767 : e);
               if (W <= 0 || (vl - 1) / W == w0 + w) lst.push_back(e);
             }
           if (lst.empty()) continue;
@@ -674,7 +680,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
         const int nv = nc[d - 1] + 1;
         std::vector<int64_t> off(nv + 1, 0);
         for (int32_t e : pcp[k]) {
-          const int vl = (d == 3) ? (e >> 20) & 1023 : (e >> 15) & 32767;
+          const int vl = (d == 3) ? (e >> 20) & 1023 : (d == 2 ? (e >> 15) & 32767 : e);
           ++off[vl + 1];
         }
         for (int v = 1; v <= nv; ++v) off[v] += off[v - 1];
@@ -689,7 +695,7 @@ int dg_level_create(const dg_level_desc_t* desc, const dg_tables_t* T, dg_level_
   // 2^d-patch clusters for the additive step (cluster_kernel): base vertex
   // v0 = 2a+1 per direction, colour = parity of a; only clusters with a patch
   // vertex in [pv_begin, pv_end] along the last direction
-  if (L->has_patch) {
+  if (L->has_patch && d >= 2) {
     bool ok = true;
     for (int t = 0; t < d; ++t) ok = ok && nc[t] >= 2;
     const int vlo = std::max(1, desc->pv_begin), vhi = std::min(nc[d - 1] - 1, desc->pv_end);

@@ -22,6 +22,12 @@ int fail(int code, const std::string& msg);
       return fail(DG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// device tables of a one-dimensional level (oned.cu)
+struct OneDTables {
+  const double* adiag = nullptr;  // [digit][i*n+k]
+  const double* bg = nullptr;     // [2][n]
+};
+
 // host-side launch arguments (the kernels' parameter structs are built from these)
 struct ResArgs {
   const double* x = nullptr;
@@ -33,6 +39,7 @@ struct ResArgs {
   int packed = 0;
   int block_list = 0;  // list = vertex-patch cells, 2x2x2 blocks of 8 in slot order
   double alpha = 0, beta = 0, betap = 0;
+  OneDTables oned;     // d = 1 only
   Geo geo;
 };
 
@@ -105,6 +112,8 @@ int dispatch_cell_fdm(int d, int n, const FdmArgs& p, const double* hz, const do
 int dispatch_patch_fdm(int d, int n, const FdmArgs& p, const double* hz, const double* hzt,
                        const double* heo, cudaStream_t st);
 size_t patch_fdm_scratch_bytes(int d, int n);
+int oned_residual(int n, const ResArgs& p, const OneDTables& t, cudaStream_t st);
+int oned_fdm(int n, bool patch, const FdmArgs& p, cudaStream_t st);
 bool flow_shape(int d, int n, int* gp, int* gr);
 int dispatch_flow(int d, int n, const ResArgs& ra, const FdmArgs& fa, const HostRes& h,
                   const double* hz, const double* hzt, const double* heo, const FlowDev& fd,

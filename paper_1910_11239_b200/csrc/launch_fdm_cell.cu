@@ -5,6 +5,7 @@ namespace dgb {
 
 int dispatch_cell_fdm(int d, int n, const FdmArgs& p, const double* hz,
                              const double* hzt, const double* heo, cudaStream_t st) {
+  if (d == 1) return oned_fdm(n, false, p, st);
 #define X(D, N) if (d == D && n == N) return launch_fdm<D, N, false>(p, hz, hzt, heo, st);
   DG_N_CASES(X, 2)
   DG_N_CASES(X, 3)

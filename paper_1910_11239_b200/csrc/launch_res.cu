@@ -175,6 +175,7 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
 
 int dispatch_residual(int d, int n, const ResArgs& p, const HostRes& h,
                              cudaStream_t st) {
+  if (d == 1) return oned_residual(n, p, p.oned, st);
 #define X(D, N) if (d == D && n == N) return launch_residual<D, N>(p, h, st);
   DG_N_CASES(X, 2)
   DG_N_CASES(X, 3)

@@ -1,7 +1,8 @@
 """GPU parity beyond the templated kernels: vertex patches of degree 8..15
 (generic kernel csrc/fdmg.cuh: patch tensors of 18..32 per direction, the
-3D m = 32 tensor in a global scratch slice) against the reference's golden
-steps (tests/golden/make_golden_big.py) and the pinned oracle.
+3D m = 32 tensor in a global scratch slice) and one-dimensional levels
+(csrc/oned.cu) against the reference's golden steps
+(tests/golden/make_golden_big.py) and the pinned oracle.
 
 Tolerance (north star): relative L2 <= 1e-12 in fp64; index maps bit-exact.
 """
@@ -17,8 +18,8 @@ from oracle.sipg_oracle import OracleLevel
 
 pytestmark = pytest.mark.gpu
 G = golden_big()
-STEPS = sorted({k.split("/")[0] for k in G if k.startswith("sm_") and "_1d_" not in k})
-OPS = sorted({k.split("/")[0] for k in G if k.startswith("op_") and "_1d_" not in k})
+STEPS = sorted({k.split("/")[0] for k in G if k.startswith("sm_")})
+OPS = sorted({k.split("/")[0] for k in G if k.startswith("op_")})
 
 
 def _setup(d, nc, k, kind="acs", omega=1.0):
@@ -108,3 +109,39 @@ def test_single_big_patch_solve_is_exact(d, nc, k):
     y = np.zeros(o.ndofs)
     pset.solve_scaled_into(y, r, np.array([0]), 1.0)
     assert rel(a[np.ix_(gi, gi)] @ y[gi], r[gi]) <= 1e-10
+
+
+@pytest.mark.parametrize("kind,nc,k,omega,rev", [
+    ("acs", 33, 2, 0.7, False), ("mcs", 17, 15, 1.0, True), ("avs", 40, 7, 0.5, False),
+    ("mvs", 25, 4, 1.0, False), ("mvs", 2, 15, 1.0, False), ("avs", 3, 1, 0.5, False),
+])
+def test_step_1d_matches_oracle(kind, nc, k, omega, rev):
+    ctx, _, sm = _setup(1, nc, k, kind, omega)
+    x0, b = inputs(ctx.ndofs, 3)
+    x = torch.from_numpy(x0).cuda()
+    sm.smooth(x, torch.from_numpy(b).cuda(), reverse=rev)
+    want = OracleLevel((nc,), k).smooth(kind, omega, x0, b, reverse=rev)
+    got = x.cpu().numpy()
+    assert rel(got, want) <= RTOL
+    assert rel(got - x0, want - x0) <= 1e-11
+
+
+def test_1d_gather_map_and_solver_sets():
+    nc, k = 9, 5
+    lvl = dg.build_hierarchy(1, nc, 0).levels[0]
+    basis = dg.Basis1D.make(k)
+    o = OracleLevel((nc,), k)
+    pset = fd.PatchSolverSet(lvl, basis, 1.0)
+    assert np.array_equal(pset.gather_map(np.arange(len(pset.patches))),
+                          o.patch_map(o.patch_vertices()))
+    _, r = inputs(o.ndofs, 7)
+    x = np.zeros(o.ndofs)
+    pset.solve_scaled_into(x, r, None, 0.5, safe_accumulate=True)
+    want = np.zeros(o.ndofs)
+    o.patch_solve(want, r, 0.5, safe=True)
+    assert rel(x, want) <= RTOL
+    x = np.zeros(o.ndofs)
+    fd.CellSolverSet(lvl, basis, 1.0).solve_scaled_into(x, r, None, 1.0)
+    want = np.zeros(o.ndofs)
+    o.cell_solve(want, r, 1.0)
+    assert rel(x, want) <= RTOL
