@@ -197,6 +197,27 @@ int dg_prolongate(int dim, int degree, const int* coarse_cells, const double* e0
 int dg_restrict(int dim, int degree, const int* coarse_cells, const double* e0,
                 const double* e1, const double* xf, double* xc, void* stream);
 
+/* Setup-side tensor kernels (csrc/coarse.cu).  All pointers are device fp64.
+ * dg_mode_contract: out[o,i,r] = sum_k S(i,k) in[o,k,r] for a tensor viewed as
+ *   (outer, K, inner) -> (outer, I, inner); S is I x K row-major, or K x I
+ *   row-major when transposed != 0.  One mode of a sum-factorised product:
+ *   the load vector's basis contractions (`_tensor.backward_all`,
+ *   _tensor.py:81-97, called by compute_rhs, dgop.py:800-871) and the passes
+ *   of the coarse solve below.
+ * dg_canonical_tensor: canonical cell-major vector (dgop.py:70-103) <->
+ *   direction-major global tensor T[j_1 + N_1 (j_2 + N_2 j_3)], j_t = c_t n + i_t,
+ *   N_t = ncells[t] n (to_tensor != 0: canonical -> tensor).
+ * dg_kron_scale: T[j] /= lam0[j_1] + lam1[j_2] + lam2[j_3] (null = absent).
+ * Together they apply A^-1 = (x)Z diag(1/sum lambda) (x)Z^T with the global
+ * 1D eigenpairs of a Cartesian level: the exact coarse solve that stands in
+ * for CoarseSolver's dense Cholesky / sparse LU (multigrid.py:169-195).      */
+int dg_mode_contract(const double* in, double* out, const double* S, int64_t outer, int K,
+                     int I, int64_t inner, int transposed, void* stream);
+int dg_canonical_tensor(int dim, int degree, const int* ncells, const double* in, double* out,
+                        int to_tensor, void* stream);
+int dg_kron_scale(double* tensor, const double* lam0, const double* lam1, const double* lam2,
+                  int n0, int n1, int n2, void* stream);
+
 /* Fused vector kernels of the device-resident CG (krylov.pcg,
  * krylov.py:69-123).  `part` is device scratch of >= 1024 doubles, `out` one
  * device double receiving the (deterministic, fixed-order) reduction.

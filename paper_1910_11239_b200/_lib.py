@@ -31,6 +31,7 @@ EXPORTS = (
     "dg_build_flags",
     "dg_prolongate", "dg_restrict", "dg_cg_update", "dg_xpby", "dg_dot", "dg_solve_range",
     "dg_mvs_range", "dg_dist_apply", "dg_dist_cell_fdm",
+    "dg_mode_contract", "dg_canonical_tensor", "dg_kron_scale",
 )
 
 
@@ -101,6 +102,9 @@ def load() -> ctypes.CDLL:
         "dg_mvs_range": ([vp, c_int, c_int, c_double, vp, vp, vp, c_int, c_int, vp], c_int),
         "dg_dist_apply": ([vp, vp, vp, vp, vp], c_int),
         "dg_dist_cell_fdm": ([c_int, c_int, i64, vp, vp, vp, vp, c_double, vp, i64, vp], c_int),
+        "dg_mode_contract": ([vp, vp, vp, i64, c_int, c_int, i64, c_int, vp], c_int),
+        "dg_canonical_tensor": ([c_int, c_int, ctypes.POINTER(c_int), vp, vp, c_int, vp], c_int),
+        "dg_kron_scale": ([vp, vp, vp, vp, c_int, c_int, c_int, vp], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

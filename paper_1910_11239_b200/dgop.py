@@ -209,6 +209,27 @@ def _coupling(t: LevelTables) -> np.ndarray:
     return a
 
 
+def global_1d_pencils(ctx: OperatorContext):
+    """Per direction the global 1D matrices (A_g, M_g) of a Cartesian level:
+    A_g block tridiagonal with A_diag(digit) on the diagonal and the rank-2
+    coupling a_pm above it, M_g = I (x) M."""
+    t = ctx.tables
+    n, dims = ctx.layout.n1d, ctx.layout.dims
+    apm = _coupling(t)
+    out = []
+    for dt in range(ctx.layout.dim):
+        nt = dims[dt]
+        a1 = np.zeros((nt * n, nt * n))
+        for c in range(nt):
+            digit = (1 if c == 0 else 0) | (2 if c == nt - 1 else 0)
+            a1[c * n:(c + 1) * n, c * n:(c + 1) * n] = t.adiag[digit]
+            if c + 1 < nt:
+                a1[c * n:(c + 1) * n, (c + 1) * n:(c + 2) * n] = apm
+                a1[(c + 1) * n:(c + 2) * n, c * n:(c + 1) * n] = apm.T
+        out.append((a1, np.kron(np.eye(nt), t.mass)))
+    return out
+
+
 def assemble_dense(ctx: OperatorContext, via: str = "kronecker", device=None):
     """Dense level matrix in the canonical layout (cf. `dgop.py:1045-1072`),
     for coarse levels: on a Cartesian level A = sum_t M (x) .. A_g^(t) .. (x) M
@@ -230,21 +251,12 @@ def assemble_dense(ctx: OperatorContext, via: str = "kronecker", device=None):
         return a.numpy() if device is None else a
     if via not in ("kronecker", "quadrature"):
         raise ValueError("via must be 'kronecker', 'quadrature' or 'matvec'")
-    t = ctx.tables
-    n, d, dims = lay.n1d, lay.dim, lay.dims
-    apm = _coupling(t)
+    d = lay.dim
+    n, dims = lay.n1d, lay.dims
     ag, mg = [], []
-    for dt in range(d):
-        nt = dims[dt]
-        a1 = np.zeros((nt * n, nt * n))
-        for c in range(nt):
-            digit = (1 if c == 0 else 0) | (2 if c == nt - 1 else 0)
-            a1[c * n:(c + 1) * n, c * n:(c + 1) * n] = t.adiag[digit]
-            if c + 1 < nt:
-                a1[c * n:(c + 1) * n, (c + 1) * n:(c + 2) * n] = apm
-                a1[(c + 1) * n:(c + 2) * n, c * n:(c + 1) * n] = apm.T
+    for a1, m1 in global_1d_pencils(ctx):
         ag.append(torch.from_numpy(a1).to(dev))
-        mg.append(torch.from_numpy(np.kron(np.eye(nt), t.mass)).to(dev))
+        mg.append(torch.from_numpy(m1).to(dev))
     a = None
     for dt in range(d):
         term = None
@@ -267,16 +279,35 @@ def assemble_dense(ctx: OperatorContext, via: str = "kronecker", device=None):
     return a.numpy() if device is None else a
 
 
+def mode_contract(t: torch.Tensor, mat: torch.Tensor, axis: int) -> torch.Tensor:
+    """Contract `axis` of the contiguous fp64 CUDA tensor t with mat (I x K,
+    K = t.shape[axis]): out[.., i, ..] = sum_k mat[i, k] t[.., k, ..], the
+    axis staying in place (C ABI `dg_mode_contract`, csrc/coarse.cu)."""
+    from ._device import stream_handle
+    t = t.contiguous()
+    mat = mat.contiguous()
+    shape = list(t.shape)
+    k = shape[axis]
+    if mat.shape[1] != k:
+        raise ValueError("mode_contract: matrix columns must match the contracted axis")
+    outer = int(np.prod(shape[:axis], dtype=np.int64))
+    inner = int(np.prod(shape[axis + 1:], dtype=np.int64))
+    shape[axis] = mat.shape[0]
+    out = torch.empty(shape, dtype=torch.float64, device=t.device)
+    lib = _lib.load()
+    _lib.check(lib.dg_mode_contract(t.data_ptr(), out.data_ptr(), mat.data_ptr(), outer, k,
+                                    int(mat.shape[0]), inner, 0, stream_handle()))
+    return out
+
+
 def _contract_quad(w: torch.Tensor, vals: torch.Tensor, k: int) -> torch.Tensor:
     """(B, q_1..q_k) reversed quadrature layout -> (B, n_k..n_1) canonical:
     out[b, i_k..i_1] = sum_q prod_t phi_{i_t}(x_{q_t}) w[b, q_1..q_k]
-    (`_tensor.backward_all`, `_tensor.py:81-97`)."""
+    (`_tensor.backward_all`, `_tensor.py:81-97`): one hand-written mode
+    contraction per direction, then the axis reversal to the canonical order."""
     y = w
-    for _ in range(k):
-        # contract the current first quadrature axis (after the batch), append
-        # the node axis at the end, so the node axes come out n_1 .. n_k
-        y = torch.tensordot(y, vals, dims=([1], [1]))
-    # y: (B, n_1, .., n_k) -> canonical (B, n_k, .., n_1)
+    for ax in range(1, k + 1):
+        y = mode_contract(y, vals, ax)      # (B, n_1, .., n_k) when done
     return y.permute(0, *range(k, 0, -1)).contiguous() if k > 1 else y
 
 

@@ -147,6 +147,43 @@ def test_coarse_solvers_match_reference(name, d, nc, k):
     assert rel(x, G[name + "/direct"]) <= 1e-7
 
 
+@pytest.mark.parametrize("d,dims,k", [(3, (2, 2, 2), 5), (3, (3, 2, 4), 3), (2, (8, 8), 4),
+                                      (2, (5, 3), 7), (3, (1, 1, 1), 6), (1, (7,), 4),
+                                      (3, (2, 2, 2), 15), (2, (32, 32), 3)])
+def test_kronecker_fdm_coarse_solve_is_exact(d, dims, k):
+    """Direct coarse solve on Cartesian levels (global fast diagonalisation,
+    csrc/coarse.cu): A x = b to rounding, and equal to a dense solve with the
+    assembled matrix (the reference's Cholesky / LU, `multigrid.py:169-195`)."""
+    from paper_1910_11239_b200.mesh import MeshLevel
+    lvl = MeshLevel(d, tuple(dims), 1.0 / dims[0])
+    basis = dg.Basis1D.make(k)
+    ctx = dg.make_context(lvl, basis, 1.0)
+    cs = mg.CoarseSolver(ctx, basis, mg.MultigridConfig(coarse="direct"))
+    assert cs.mode == "direct" and cs.direct_kind == "kronecker_fdm"
+    b = torch.from_numpy(useed(ctx.ndofs, 3)).cuda()
+    x = torch.empty_like(b)
+    cs.solve(b, x)
+    ax = dg.apply_operator(ctx, x)
+    assert float((ax - b).norm() / b.norm()) <= 1e-11
+    if ctx.ndofs <= 6000:
+        a = dgop.assemble_dense(ctx, device="cuda")
+        want = torch.linalg.solve(a, b)
+        assert float((x - want).norm() / want.norm()) <= 1e-10
+
+
+def test_mode_contract_matches_tensordot():
+    g = torch.Generator("cuda").manual_seed(5)
+    t = torch.rand((3, 5, 7, 4), dtype=torch.float64, device="cuda", generator=g)
+    for ax, i in ((1, 6), (2, 2), (3, 9), (0, 4)):
+        m = torch.rand((i, t.shape[ax]), dtype=torch.float64, device="cuda", generator=g)
+        want = torch.movedim(torch.tensordot(t, m, dims=([ax], [1])), -1, ax)
+        got = dgop.mode_contract(t, m, ax)
+        assert got.shape == want.shape
+        assert float((got - want).abs().max()) <= 1e-13
+    with pytest.raises(ValueError):
+        dgop.mode_contract(t, torch.zeros((2, 3), dtype=torch.float64, device="cuda"), 1)
+
+
 def test_coarse_zero_rhs_and_dense_assembly():
     basis = dg.Basis1D.make(2)
     ctx = dg.make_context(dg.build_hierarchy(2, 2, 0).levels[0], basis, 1.0)
