@@ -167,6 +167,19 @@ __host__ __device__ constexpr int dist_cells() {
   return ND > 64 ? 1 : (128 / ND > 8 ? 8 : 128 / ND);
 }
 
+// shared doubles of dist_apply_kernel; large cells alias the face-phase
+// buffers with the volume-phase ones (see the kernel)
+template <int D, int N>
+__host__ __device__ constexpr bool dist_alias() {
+  constexpr size_t ND = D == 3 ? N * N * N : N * N, FT = D == 3 ? N * N : N;
+  return N >= 7 && sizeof(double) * dist_cells<D, N>() * (7 * ND + 19 * FT) > 160 * 1024;
+}
+template <int D, int N>
+__host__ __device__ constexpr size_t dist_smem_doubles() {
+  constexpr size_t ND = D == 3 ? N * N * N : N * N, FT = D == 3 ? N * N : N;
+  return dist_cells<D, N>() * (dist_alias<D, N>() ? 6 * ND : 7 * ND + 19 * FT);
+}
+
 template <int D, int N>
 __global__ void __launch_bounds__(128) dist_apply_kernel(const __grid_constant__ DistParams<D, N> P,
                                                          int64_t ncells) {
@@ -175,14 +188,19 @@ __global__ void __launch_bounds__(128) dist_apply_kernel(const __grid_constant__
   constexpr int FT = D == 3 ? N * N : N;
   constexpr int S = D == 3 ? 6 : 3;
   extern __shared__ __align__(16) double sm[];
+  // seven cell tensors plus the face scratch; for large cells (dist_alias)
+  // the face phase reuses the volume phase's dead buffers: the neighbour
+  // copy NB lives in A and the 19 face fields in B, E, F (19 n^(d-1) <= 3 n^d
+  // for n >= 7), which lets 3D n = 16 fit in 192 KB
+  constexpr bool AL = dist_alias<D, N>();
   double* U = sm;
-  double* NB = U + G * ND;
-  double* A = NB + G * ND;
-  double* B = A + G * ND;
-  double* C = B + G * ND;
-  double* E = C + G * ND;
+  double* A = U + G * ND;
+  double* C = A + G * ND;
+  double* B = C + G * ND;
+  double* E = B + G * ND;
   double* F = E + G * ND;
-  double* fs = F + G * ND;  // face scratch: 19 fields of G * FT
+  double* NB = AL ? A : F + G * ND;
+  double* fs = AL ? B : NB + G * ND;  // face scratch: 19 fields of G * FT
   __shared__ int s_c[G][3];
   __shared__ int s_ok[G];
   const int n = P.n;
@@ -660,7 +678,10 @@ __global__ void __launch_bounds__(128)
                          double omega) {
   constexpr int G = dist_cells<D, N>();
   constexpr int ND = D == 3 ? N * N * N : N * N;
-  __shared__ double T0[G * ND], T1[G * ND], Zs[G * D * N * N];
+  extern __shared__ __align__(16) double sm[];
+  double* T0 = sm;
+  double* T1 = T0 + G * ND;
+  double* Zs = T1 + G * ND;
   __shared__ int64_t s_cell[G];
   const int64_t i0 = (int64_t)blockIdx.x * G;
   if (threadIdx.x < G) {
@@ -783,8 +804,6 @@ static int launch_dist(const DistArgs& a, const double* u, const double* b, doub
       P.tab.bv[p][i] = a.bv[p * N + i];
       P.tab.bg[p][i] = a.bg[p * N + i];
     }
-  constexpr int ND = D == 3 ? N * N * N : N * N;
-  constexpr int FT = D == 3 ? N * N : N;
   int64_t ncells = 1;
   for (int t = 0; t < D; ++t) ncells *= a.ncells_dim;
   if constexpr (dist_reg_ok<D, N>()) {
@@ -795,7 +814,7 @@ static int launch_dist(const DistArgs& a, const double* u, const double* b, doub
     }
   }
   constexpr int G = dist_cells<D, N>();
-  const size_t smem = sizeof(double) * G * (7 * (size_t)ND + 19 * (size_t)FT);
+  const size_t smem = sizeof(double) * dist_smem_doubles<D, N>();
   auto k = dist_apply_kernel<D, N>;
   if (smem > 48 * 1024)
     DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -817,8 +836,12 @@ static int launch_cell_fdm(const double* r, double* x, const double* z, const do
     }
   }
   constexpr int G = dist_cells<D, N>();
-  dist_cell_fdm_kernel<D, N><<<(unsigned)((nb + G - 1) / G), 128, 0, st>>>(r, x, z, inv, cells,
-                                                                           nb, ncells, omega);
+  constexpr int ND = D == 3 ? N * N * N : N * N;
+  const size_t smem = sizeof(double) * G * (2 * (size_t)ND + D * N * N);
+  auto k = dist_cell_fdm_kernel<D, N>;
+  if (smem > 48 * 1024)
+    DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<(unsigned)((nb + G - 1) / G), 128, smem, st>>>(r, x, z, inv, cells, nb, ncells, omega);
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }
@@ -834,10 +857,10 @@ extern "C" int dg_dist_apply(const dg_dist_args_t* args, const double* u, const 
   cudaStream_t st = (cudaStream_t)stream;
 #define DG_DCASE(D, NN) \
   if (a.dim == D && n == NN) return launch_dist<D, NN>(a, u, b, out, st);
-  DG_DCASE(2, 2) DG_DCASE(2, 3) DG_DCASE(2, 4) DG_DCASE(2, 5) DG_DCASE(2, 6) DG_DCASE(2, 7)
-  DG_DCASE(2, 8) DG_DCASE(3, 2) DG_DCASE(3, 3) DG_DCASE(3, 4) DG_DCASE(3, 5) DG_DCASE(3, 6)
+  DG_N_CASES(DG_DCASE, 2)
+  DG_N_CASES(DG_DCASE, 3)
 #undef DG_DCASE
-  return fail(DG_EUNSUPPORTED, "distorted operator: dim 2 (k <= 7) or 3 (k <= 5)");
+  return fail(DG_EUNSUPPORTED, "distorted operator: dim 2 or 3, degree 1..15");
 }
 
 extern "C" int dg_dist_cell_fdm(int dim, int degree, int64_t ncells, const double* z,
@@ -852,8 +875,8 @@ extern "C" int dg_dist_cell_fdm(int dim, int degree, int64_t ncells, const doubl
   cudaStream_t st = (cudaStream_t)stream;
 #define DG_FCASE(D, NN) \
   if (dim == D && n == NN) return launch_cell_fdm<D, NN>(r, x, z, inv, cells, nb, ncells, omega, st);
-  DG_FCASE(2, 2) DG_FCASE(2, 3) DG_FCASE(2, 4) DG_FCASE(2, 5) DG_FCASE(2, 6) DG_FCASE(2, 7)
-  DG_FCASE(2, 8) DG_FCASE(3, 2) DG_FCASE(3, 3) DG_FCASE(3, 4) DG_FCASE(3, 5) DG_FCASE(3, 6)
+  DG_N_CASES(DG_FCASE, 2)
+  DG_N_CASES(DG_FCASE, 3)
 #undef DG_FCASE
-  return fail(DG_EUNSUPPORTED, "surrogate cell solve: dim 2 (k <= 7) or 3 (k <= 5)");
+  return fail(DG_EUNSUPPORTED, "surrogate cell solve: dim 2 or 3, degree 1..15");
 }
