@@ -331,7 +331,7 @@ def test_patch_degree_above_templates_is_supported():
     basis = dg.Basis1D.make(8)
     ctx = dg.make_context(lvl, basis)
     sm = dg.make_level_smoother(ctx, basis, dg.SmootherConfig("avs", 0.25))
-    assert sm.solvers.m1 == 18
+    assert sm.set.m1 == 18
 
 
 @experimental
