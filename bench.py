@@ -311,7 +311,11 @@ def run_ours(args, cfg):
                 os.environ.setdefault("MASTER_PORT", "29531")
                 os.environ.setdefault("RANK", "0")
                 os.environ.setdefault("WORLD_SIZE", "1")
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            # a dead peer fails the run after 5 minutes instead of NCCL's 10-minute
+            # default hanging the box (the halo exchange is the only traffic)
+            import datetime
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                    timeout=datetime.timedelta(minutes=5))
     d, nc, k, kind, omega = cfg["d"], cfg["nc"], cfg["k"], cfg["kind"], cfg["omega"]
     if slab and args.config != 5:
         raise SystemExit("multi-GPU (slab) runs use the cfg-5 weak-scaling workload")

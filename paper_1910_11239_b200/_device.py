@@ -9,6 +9,8 @@ float64 CUDA tensors (zero-copy, ordered on the current stream).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -84,3 +86,27 @@ class Staged:
                 return
             out = self.dev.cpu().numpy()
             np.copyto(self.host, out.reshape(self.host.shape))
+
+
+_NVTX = os.environ.get("DGB_NVTX", "0") != "0"
+
+
+class nvtx_range:
+    """NVTX range around a public call when DGB_NVTX=1 (the profilers' timeline
+    then shows smoothing steps, V-cycles and Krylov solves by name); a no-op
+    otherwise."""
+
+    __slots__ = ("name",)
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        if _NVTX:
+            torch.cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
+        return False

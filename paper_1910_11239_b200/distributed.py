@@ -122,8 +122,13 @@ def halo_exchange(vec: torch.Tensor, layout: SlabLayout, group=None) -> None:
     for peer, send, recv in plan:
         ops.append(dist.P2POp(dist.isend, vec[send], peer, group))
         ops.append(dist.P2POp(dist.irecv, vec[recv], peer, group))
-    for w in dist.batch_isend_irecv(ops):
-        w.wait()
+    try:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    except RuntimeError as e:  # NCCL / gloo timeout or a dead peer: say which exchange failed
+        peers = sorted({peer for peer, _, _ in plan})
+        raise RuntimeError(f"halo exchange of rank {layout.rank} with rank(s) {peers} failed "
+                           f"({sum(vec[s].numel() for _, s, _ in plan) * 8} bytes sent): {e}") from e
 
 
 class SlabSmoother:
