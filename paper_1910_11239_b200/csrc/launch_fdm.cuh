@@ -16,6 +16,10 @@
 #include "fdm_mma.cuh"
 #endif
 
+#ifdef DGB_EXPERIMENTAL
+#include "fdm7.cuh"
+#endif
+
 #include <algorithm>
 #include <cstring>
 
@@ -174,6 +178,27 @@ static int launch_fdm(const FdmArgs& q, const double* hz, const double* hzt, con
         const int64_t ngp = (q.count + SP::G - 1) / SP::G;
         DG_CUDA(cudaMemsetAsync(q.counter, 0, sizeof(int), st));
         kp<<<(unsigned)std::min<int64_t>(ngp, residentp), SP::NT, smemp, st>>>(p, ngp, q.counter);
+        DG_CUDA(cudaGetLastError());
+        return DG_OK;
+      }
+    }
+#endif
+#ifdef DGB_EXPERIMENTAL
+    if constexpr (PATCH && D == 3 && M == 12) {
+      // two fibers per thread (fdm7.cuh): measured slower (2.43 vs 1.79 ms at
+      // cfg 5 with two CTAs of 288 threads per SM, 4.24 ms with one), opt-in
+      const int v7 = env_int("DGB_FDM7", 0);
+      if (v7 && p.direct == 2 && (!q.atomic || env_int("DGB_BULK_ATOMIC", 1)) && !q.cluster) {
+        using S7 = Fdm7Shape<M>;
+        auto k7 = v7 == 1 ? fdm7_kernel<M, 96> : fdm7_kernel<M, 128>;
+        const size_t smem7 = sizeof(double) * S7::SMEM;
+        static bool attr7[2] = {false, false};
+        if (!attr7[v7 == 1]) {
+          DG_CUDA(cudaFuncSetAttribute(k7, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem7));
+          DG_CUDA(cudaFuncSetAttribute(k7, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+          attr7[v7 == 1] = true;
+        }
+        k7<<<(unsigned)((q.count + S7::G - 1) / S7::G), S7::NT, smem7, st>>>(p);
         DG_CUDA(cudaGetLastError());
         return DG_OK;
       }
