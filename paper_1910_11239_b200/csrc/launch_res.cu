@@ -161,12 +161,15 @@ static int launch_residual(const ResArgs& q, const HostRes& h, cudaStream_t st) 
     }
   }
 #endif
-  const size_t smem = sizeof(double) * res2_smem_doubles<D, N>();
+  size_t smem = sizeof(double) * res2_smem_doubles<D, N>();
+#ifdef DGB_EXPERIMENTAL
+  smem += (size_t)env_int("DGB_RES2_PAD", 0);  // occupancy experiment: extra bytes per CTA
+#endif
   auto k = res2_kernel<D, N>;
-  static bool attr = false;
-  if (!attr) {
+  static size_t attr = 0;
+  if (attr < smem) {
     DG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+    attr = smem;
   }
   k<<<(unsigned)ngroups, NT, smem, st>>>(p);
   DG_CUDA(cudaGetLastError());
