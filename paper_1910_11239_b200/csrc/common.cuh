@@ -100,6 +100,9 @@ __host__ __device__ constexpr int fdm2_groups() {
 #ifdef FDM_G12
   if (D == 3 && M == 12) return FDM_G12;
 #endif
+#ifdef FDM_G8
+  if (D == 3 && M == 8) return FDM_G8;
+#endif
   for (int g = 1; g <= 32; ++g)
     if ((g * F) % 32 == 0 && g * F >= 128 && g * F <= 512) return g;
   return F >= 128 ? 1 : (128 + F - 1) / F;
