@@ -485,17 +485,31 @@ def run_ours(args, cfg):
         e2e["frac_of_copy_bound"] = c_ms / e_ms
         # the reference's own callers pass pageable numpy arrays: the same
         # call on those (the copies go through the driver's staging buffers)
+        # (first call: pageable copies; second call: the recurring buffers are
+        # page-locked in place, _device.maybe_pin, its cost is in that call;
+        # after that the call runs the pinned pipeline)
         xn, bn = x_h.copy(), b_h.copy()
-        sm.smooth(xn, bn)
+        calls = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            sm.smooth(xn, bn)
+            calls.append((time.perf_counter() - t0) * 1e3)
         torch.cuda.synchronize()
         kp = max(2, min(args.steps, 5))
         t0 = time.perf_counter()
         for _ in range(kp):
             sm.smooth(xn, bn)
         p_ms = (time.perf_counter() - t0) * 1e3 / kp
+        from paper_1910_11239_b200 import _device
         e2e["pageable"] = {"value": n_global / (p_ms * 1e-3), "unit": "DoF/s", "ms_per_step": p_ms,
-                           "api": "LevelSmoother.smooth(numpy float64 arrays, pageable)",
-                           "timing": "host wall clock around the call (it returns with x final)"}
+                           "first_call_ms": calls[0], "second_call_ms": calls[1],
+                           "page_locked_in_place": bool(_device._pin_live),
+                           "api": "LevelSmoother.smooth(numpy float64 arrays), the same arrays "
+                                  "on every call as the reference's V-cycle passes them",
+                           "timing": "host wall clock around the call (it returns with x final); "
+                                     "first_call = pageable copies, second_call includes the "
+                                     "in-place cudaHostRegister of x and b, ms_per_step = the "
+                                     "calls after that"}
         del xn, bn
     else:
         e2e = step_obj.e2e(x_h, b_h, reps=max(3, min(args.steps, 10)))

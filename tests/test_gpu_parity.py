@@ -600,3 +600,42 @@ def test_mvs_host_wavefront_pipeline_bitwise(k, nc, rev, monkeypatch):
         xh.copy_(torch.from_numpy(x0))
         sm.smooth(xh, bh, reverse=rev)
         assert np.array_equal(xh.numpy(), want)
+
+
+def test_recurring_numpy_buffers_are_page_locked_in_place(monkeypatch):
+    """The same numpy arrays passed a second time are registered in place
+    (cudaHostRegister): results are unchanged, the later calls take the pinned
+    pipeline, and the registration goes away with the array."""
+    import gc
+    from paper_1910_11239_b200 import _device
+    monkeypatch.setattr(_device, "_PIN_MODE", "auto")
+    monkeypatch.setattr(_device, "_PIN_MIN_BYTES", 1 << 16)
+    ctx, _, sm = _setup(3, 12, 3, "avs", 0.25)
+    x0, b = inputs(ctx.ndofs, 5)
+    want = x0.copy()
+    xd = torch.from_numpy(x0).cuda()
+    sm.smooth(xd, torch.from_numpy(b).cuda())
+    want = xd.cpu().numpy()
+    x = x0.copy()
+    ptr = x.ctypes.data
+    sm.smooth(x, b)                         # first sighting: pageable
+    assert ptr not in _device._pin_live
+    assert rel(x, want) <= 1e-14
+    x[:] = x0
+    sm.smooth(x, b)                         # second sighting: registered
+    assert _device._pin_live.get(ptr) == x.nbytes
+    assert torch.from_numpy(x).is_pinned()
+    assert rel(x, want) <= 1e-14
+    x[:] = x0
+    sm.smooth(x, b)
+    assert rel(x, want) <= 1e-14
+    v = x[: ctx.ndofs // 2]                  # a view does not own the memory
+    del v
+    del x
+    gc.collect()
+    assert ptr not in _device._pin_live
+    # read-only and small arrays are left alone
+    ro = b.copy()
+    ro.flags.writeable = False
+    assert not _device.maybe_pin(ro) and not _device.maybe_pin(ro)
+    assert not _device.maybe_pin(np.zeros(8)) and not _device.maybe_pin(np.zeros(8))
