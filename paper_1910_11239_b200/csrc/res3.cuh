@@ -18,6 +18,12 @@
 
 namespace dgb {
 
+// the right-hand side fiber of the last pass is prefetched across the barrier
+// for n > RES3_BPRE_MIN (16 more live registers in pass 1)
+#ifndef RES3_BPRE_MIN
+#define RES3_BPRE_MIN 6
+#endif
+
 template <int N>
 struct Res3Shape {
   using L = Lay<3, N>;
@@ -147,7 +153,7 @@ __device__ __forceinline__ void res3_tail(const Res2Params<3, N>& p, bool active
     for (int k = 0; k < N; ++k) A[sb + k * ss] = o[k] + t[k];
     // right-hand side along the t = 2 fiber (i0, i1) = (fa, fb), prefetched
     // across the barrier (n <= 6: loaded in the last pass, fewer registers)
-    if (N > 6 && p.b) {
+    if (N > RES3_BPRE_MIN && p.b) {
 #pragma unroll
       for (int k = 0; k < N; ++k) bq[k] = __ldg(p.b + cb + fa + N * fb + N * N * k);
     }
@@ -168,7 +174,7 @@ __device__ __forceinline__ void res3_tail(const Res2Params<3, N>& p, bool active
     for (int k = 0; k < N; ++k) v[k] = A[sb + k * ss];
     mass3<N>(p, v, o);        // M_2 c
     double* r = p.r + cb + fa + N * fb;
-    if (N <= 6 && p.b) {
+    if (N <= RES3_BPRE_MIN && p.b) {
 #pragma unroll
       for (int k = 0; k < N; ++k) bq[k] = __ldg(p.b + cb + fa + N * fb + N * N * k);
     }
