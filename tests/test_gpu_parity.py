@@ -639,3 +639,51 @@ def test_recurring_numpy_buffers_are_page_locked_in_place(monkeypatch):
     ro.flags.writeable = False
     assert not _device.maybe_pin(ro) and not _device.maybe_pin(ro)
     assert not _device.maybe_pin(np.zeros(8)) and not _device.maybe_pin(np.zeros(8))
+
+
+@experimental
+@pytest.mark.parametrize("k,nc,kind", [(7, 6, "mvs"), (15, 3, "acs"), (5, 6, "avs"), (7, 5, "acs")])
+def test_res3_load_variants_bitwise(k, nc, kind, monkeypatch):
+    """res3b (batched neighbour-fiber loads) and res3c (TMA-staged rows, pair
+    mode on patch-cell lists) keep res3's arithmetic: bitwise equal residuals
+    and smoothing steps (the variants are opt-in: measured no faster)."""
+    monkeypatch.setenv("DGB_RES3_LO", "1")     # n = 6 on res3 too
+    monkeypatch.setenv("DGB_HOST_PIPELINE", "0")
+    got = {}
+    for name, env in (("res3", {}), ("res3b", {"DGB_RES3_BATCH": "1"}),
+                      ("res3c", {"DGB_RES3_TMA": "1"})):
+        for kk in ("DGB_RES3_BATCH", "DGB_RES3_TMA"):
+            monkeypatch.delenv(kk, raising=False)
+        for kk, v in env.items():
+            monkeypatch.setenv(kk, v)
+        ctx, _, sm = _setup(3, nc, k, kind, 0.25 if kind == "avs" else 1.0)
+        x0, b = inputs(ctx.ndofs, 9)
+        r = dg.residual(ctx, x0, b, out=np.empty(ctx.ndofs))
+        x = x0.copy()
+        sm.use_graph = False
+        sm.smooth(x, b)
+        got[name] = (r, x)
+    for name in ("res3b", "res3c"):
+        assert np.array_equal(got[name][0], got["res3"][0])
+        if kind != "avs":   # the default AVS path sums its updates in arbitrary order
+            assert np.array_equal(got[name][1], got["res3"][1])
+        else:
+            assert rel(got[name][1], got["res3"][1]) <= 1e-14
+
+
+@experimental
+def test_two_fiber_patch_solve_matches_default(monkeypatch):
+    """fdm7 (two fibers per thread, opt-in) against the default bulk solve on
+    the cfg-5 discretisation, colour by colour (deterministic order): bitwise."""
+    monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
+    monkeypatch.setenv("DGB_HOST_PIPELINE", "0")
+    out = {}
+    for v in ("0", "1", "2"):
+        monkeypatch.setenv("DGB_FDM7", v)
+        ctx, _, sm = _setup(3, 7, 5, "avs", 0.25)
+        x0, b = inputs(ctx.ndofs, 4)
+        x = x0.copy()
+        sm.use_graph = False
+        sm.smooth(x, b)
+        out[v] = x
+    assert np.array_equal(out["1"], out["0"]) and np.array_equal(out["2"], out["0"])
