@@ -1097,8 +1097,24 @@ static int smooth_launches(dg_level_t* L, int kind, double omega, int reverse, d
     case DG_MVS: {
       if (!L->has_patch) return fail(DG_EUNSUPPORTED, "vertex patches unsupported here");
       const int nc = (int)L->pcol_pk.size();
+      // one launch per colour with the restricted residual fused into the
+      // patch solve (mvs_fused.cuh; experimental builds, DGB_MVS_FUSED=1):
+      // bitwise the two-launch sweep, measured slower (cfg 3: 2.27 vs 2.05 ms)
+      const bool fused = mvs_fused_supported(L->d, L->n) && env_int("DGB_MVS_FUSED", 0);
       for (int i = 0; i < nc; ++i) {
         const int k = reverse ? nc - 1 - i : i;
+        if (fused) {
+          *nl += 1;
+          ResArgs ra = res_params(L, x, b, r);
+          FdmArgs fa = fdm_params(L, true, r, x, omega);
+          fa.list = L->pcol_pk[k].ptr;
+          fa.count = L->pcol_pk[k].count;
+          fa.packed = 1;
+          if ((rc = dispatch_mvs_fused(L->d, L->n, ra, fa, L->hres(), L->hpz.data(),
+                                       L->hpzt.data(), L->peo(), st)))
+            return rc;
+          continue;
+        }
         *nl += 2;
         if ((rc = res_packed(L, x, b, r, L->pcol_cells_pk[k], st, 1))) return rc;
         if ((rc = patch_fdm_packed(L, r, x, omega, L->pcol_pk[k], st))) return rc;

@@ -112,6 +112,9 @@ int dispatch_cell_fdm(int d, int n, const FdmArgs& p, const double* hz, const do
 int dispatch_patch_fdm(int d, int n, const FdmArgs& p, const double* hz, const double* hzt,
                        const double* heo, cudaStream_t st);
 size_t patch_fdm_scratch_bytes(int d, int n);
+bool mvs_fused_supported(int d, int n);
+int dispatch_mvs_fused(int d, int n, const ResArgs& ra, const FdmArgs& fa, const HostRes& h,
+                       const double* hz, const double* hzt, const double* heo, cudaStream_t st);
 int oned_residual(int n, const ResArgs& p, const OneDTables& t, cudaStream_t st);
 int oned_fdm(int n, bool patch, const FdmArgs& p, cudaStream_t st);
 bool flow_shape(int d, int n, int* gp, int* gr);

@@ -101,10 +101,10 @@ __device__ __forceinline__ void mass3(const Res2Params<3, N>& p, const double (&
 }
 
 // passes t = 1, 2 and the face-field transforms (after pass 0 and a barrier)
-template <int N>
-__device__ __forceinline__ void res3_tail(const Res2Params<3, N>& p, bool active, int f, int fa,
-                                          int fb, const int (&dig)[3], int64_t cb, double* A,
-                                          double* B, double* F1, double* F2) {
+template <int N, class Sink>
+__device__ __forceinline__ void res3_tail_to(const Res2Params<3, N>& p, bool active, int f, int fa,
+                                             int fb, const int (&dig)[3], int64_t cb, double* A,
+                                             double* B, double* F1, double* F2, Sink sink) {
   using S = Res3Shape<N>;
   using L = Lay<3, N>;
   constexpr int F = S::F;
@@ -173,7 +173,6 @@ __device__ __forceinline__ void res3_tail(const Res2Params<3, N>& p, bool active
 #pragma unroll
     for (int k = 0; k < N; ++k) v[k] = A[sb + k * ss];
     mass3<N>(p, v, o);        // M_2 c
-    double* r = p.r + cb + fa + N * fb;
     if (N <= RES3_BPRE_MIN && p.b) {
 #pragma unroll
       for (int k = 0; k < N; ++k) bq[k] = __ldg(p.b + cb + fa + N * fb + N * N * k);
@@ -181,39 +180,32 @@ __device__ __forceinline__ void res3_tail(const Res2Params<3, N>& p, bool active
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       const double ax = o[k] + t[k];
-      r[N * N * k] = p.b ? bq[k] - ax : ax;
+      sink(k, p.b ? bq[k] - ax : ax);  // entry (i0, i1, i2) = (fa, fb, k) of the cell
     }
   }
 }
 
-template <int N, int MINB>
-__global__ void __launch_bounds__(Res3Shape<N>::NT, MINB)
-res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
+// ... with r = b - A x (or A x) written to global memory
+template <int N>
+__device__ __forceinline__ void res3_tail(const Res2Params<3, N>& p, bool active, int f, int fa,
+                                          int fb, const int (&dig)[3], int64_t cb, double* A,
+                                          double* B, double* F1, double* F2) {
+  double* r = p.r + cb + fa + N * fb;
+  res3_tail_to<N>(p, active, f, fa, fb, dig, cb, A, B, F1, F2,
+                  [&](int k, double v) { r[N * N * k] = v; });
+}
+
+// pass t = 0 of one cell (own row from global memory, the two direction-0
+// neighbour rows) and the raw face fields of directions 1 and 2
+template <int N>
+__device__ __forceinline__ void res3_pass0(const Res2Params<3, N>& p, bool active, int f, int fa,
+                                           int fb, const int (&c)[3], const int (&dig)[3],
+                                           int64_t cb, double* A, double* B, double* F1,
+                                           double* F2) {
   using S = Res3Shape<N>;
   using L = Lay<3, N>;
-  constexpr int G = S::G, F = S::F, NE = L::NE;
-  extern __shared__ __align__(16) double sm[];
-  __shared__ int s_cell[G];
-  __shared__ int s_c[G][3];
-  const int tid = threadIdx.x;
-  if (tid < G)
-    s_cell[tid] = res_cell<3>(p.geo, p.list, p.packed, p.start, p.count,
-                              (int64_t)blockIdx.x * G + tid, s_c[tid]);
-  __syncthreads();
-  const int g = tid / F, f = tid - g * F;
-  const int cell = s_cell[g];
-  const bool active = cell >= 0;
-  int c[3] = {s_c[g][0], s_c[g][1], s_c[g][2]};
-  int dig[3];
-#pragma unroll
-  for (int t = 0; t < 3; ++t) dig[t] = (c[t] == 0 ? 1 : 0) | (c[t] == p.geo.nc[t] - 1 ? 2 : 0);
-  double* A = sm + g * S::CS;
-  double* B = A + L::SZ;
-  double* F1 = B + L::SZ;      // F1[q][i2][i0]: faces along t = 1
-  double* F2 = F1 + 4 * S::FP;  // F2[q][i1][i0]: faces along t = 2
+  constexpr int NE = L::NE;
   constexpr int FP = S::FP, NP = S::NP;
-  const int fa = f % N, fb = f / N;
-  const int64_t cb = (int64_t)(active ? cell : 0) * NE;
   auto nbr = [&](int t, int dir) -> const double* {  // neighbour cell data or null
     if (dir > 0 ? (dig[t] & 2) : (dig[t] & 1)) return nullptr;
     int nb[3] = {c[0], c[1], c[2]};
@@ -277,6 +269,37 @@ res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
       for (int q = 0; q < 4; ++q) F2[q * FP + fb * NP + fa] = fq[q];
     }
   }
+}
+
+template <int N, int MINB>
+__global__ void __launch_bounds__(Res3Shape<N>::NT, MINB)
+res3_kernel(const __grid_constant__ Res2Params<3, N> p) {
+  using S = Res3Shape<N>;
+  using L = Lay<3, N>;
+  constexpr int G = S::G, F = S::F, NE = L::NE;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_cell[G];
+  __shared__ int s_c[G][3];
+  const int tid = threadIdx.x;
+  if (tid < G)
+    s_cell[tid] = res_cell<3>(p.geo, p.list, p.packed, p.start, p.count,
+                              (int64_t)blockIdx.x * G + tid, s_c[tid]);
+  __syncthreads();
+  const int g = tid / F, f = tid - g * F;
+  const int cell = s_cell[g];
+  const bool active = cell >= 0;
+  int c[3] = {s_c[g][0], s_c[g][1], s_c[g][2]};
+  int dig[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) dig[t] = (c[t] == 0 ? 1 : 0) | (c[t] == p.geo.nc[t] - 1 ? 2 : 0);
+  double* A = sm + g * S::CS;
+  double* B = A + L::SZ;
+  double* F1 = B + L::SZ;      // F1[q][i2][i0]: faces along t = 1
+  double* F2 = F1 + 4 * S::FP;  // F2[q][i1][i0]: faces along t = 2
+  constexpr int FP = S::FP, NP = S::NP;
+  const int fa = f % N, fb = f / N;
+  const int64_t cb = (int64_t)(active ? cell : 0) * NE;
+  res3_pass0<N>(p, active, f, fa, fb, c, dig, cb, A, B, F1, F2);
   __syncthreads();
   res3_tail<N>(p, active, f, fa, fb, dig, cb, A, B, F1, F2);
 }

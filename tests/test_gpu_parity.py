@@ -687,3 +687,23 @@ def test_two_fiber_patch_solve_matches_default(monkeypatch):
         sm.smooth(x, b)
         out[v] = x
     assert np.array_equal(out["1"], out["0"]) and np.array_equal(out["2"], out["0"])
+
+
+@experimental
+@pytest.mark.parametrize("nc,rev", [(2, False), (5, False), (4, True)])
+def test_fused_mvs_colour_kernel_bitwise(nc, rev, monkeypatch):
+    """mvs_fused_kernel (restricted residual + patch solve per patch, opt-in)
+    against the two-launch sweep on 3D Q7: bitwise, and the oracle at 1e-12."""
+    monkeypatch.setenv("DGB_HOST_PIPELINE", "0")
+    out = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv("DGB_MVS_FUSED", v)
+        ctx, _, sm = _setup(3, nc, 7, "mvs", 1.0)
+        x0, b = inputs(ctx.ndofs, 2)
+        x = x0.copy()
+        sm.use_graph = False
+        sm.smooth(x, b, reverse=rev)
+        out[v] = x
+    assert np.array_equal(out["0"], out["1"])
+    want = OracleLevel((nc,) * 3, 7).smooth("mvs", 1.0, x0, b, reverse=rev)
+    assert rel(out["1"], want) <= RTOL
