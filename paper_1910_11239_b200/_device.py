@@ -53,12 +53,40 @@ def _owner(arr: np.ndarray):
     return o
 
 
+_pin_pending: list = []            # unregistrations deferred out of a stream capture
+
+
+def _capturing() -> bool:
+    try:
+        return torch.cuda.is_current_stream_capturing()
+    except Exception:
+        return False
+
+
 def _unregister(ptr: int) -> None:
-    if _pin_live.pop(ptr, None) is not None:
-        try:
-            torch.cuda.cudart().cudaHostUnregister(ptr)
-        except Exception:  # interpreter shutdown: the context may be gone
-            pass
+    """Finalizer of a registered array's owner.  It can fire at any point of
+    the Python code, also inside a `torch.cuda.graph` capture, where
+    cudaHostUnregister would invalidate the capture: deferred then."""
+    if ptr not in _pin_live:
+        return
+    if _capturing():
+        _pin_pending.append(ptr)
+        return
+    _pin_live.pop(ptr, None)
+    try:
+        torch.cuda.cudart().cudaHostUnregister(ptr)
+    except Exception:  # interpreter shutdown: the context may be gone
+        pass
+
+
+def _drain_pending() -> None:
+    while _pin_pending and not _capturing():
+        ptr = _pin_pending.pop()
+        if _pin_live.pop(ptr, None) is not None:
+            try:
+                torch.cuda.cudart().cudaHostUnregister(ptr)
+            except Exception:
+                pass
 
 
 def maybe_pin(arr) -> bool:
@@ -66,10 +94,15 @@ def maybe_pin(arr) -> bool:
     (now) page-locked.  Never raises: on any failure the array stays pageable."""
     if _PIN_MODE == "0" or not isinstance(arr, np.ndarray):
         return False
+    if _capturing():
+        return False  # no registration calls inside a stream capture
+    _drain_pending()
     if (arr.dtype != np.float64 or not arr.flags.c_contiguous or not arr.flags.writeable
             or arr.nbytes < _PIN_MIN_BYTES):
         return False
     ptr, nbytes = arr.ctypes.data, arr.nbytes
+    if ptr in _pin_pending:
+        return False  # a dead array's range waiting to be unregistered
     if _pin_live.get(ptr) == nbytes:
         return True
     key = (ptr, nbytes)
