@@ -11,8 +11,9 @@
 // one subdomain, its threads loop over the fibers, and the m^d tensor lives
 // in shared memory (pitch m+1) while it fits (m <= 30 in 3D) or in a
 // per-CTA slice of a global scratch buffer (3D m = 32: 256 KB).
-// Throughput is not the point of this path (no even/odd split, no bulk
-// copies); parity with the reference at every degree is.
+// The interior digit takes the even/odd split (half blocks from global
+// memory).  Throughput is not the point of this path (no bulk copies, one
+// CTA per patch); parity with the reference at every degree is.
 #pragma once
 #include "common.cuh"
 #include "fdm2.cuh"
@@ -28,6 +29,7 @@ struct FdmgParams {
   const double* invsum;  // [class][m^d], canonical patch order
   const double* z;       // [digit][k*m + i] = Z[k][i]   (out = Z^T v)
   const double* zt;      // [digit][k*m + i] = Z[i][k]   (out = Z v)
+  const double* eo;      // even/odd halves of the interior digit (4 x (m/2)^2) or nullptr
   double omega;
   int atomic;
   int packed;
@@ -59,6 +61,72 @@ __device__ __forceinline__ void matvec_g(const double* __restrict__ S, const dou
       o[i + 1] = fma(a.y, v[k], o[i + 1]);
     }
   }
+}
+
+// even/odd forms of the interior digit (fdm2.cuh matvec_eo_fwd / _bwd) with
+// the half blocks in global memory: half the FMAs and half the loads
+template <int M>
+__device__ __forceinline__ void matvec_eo_fwd_g(const double* __restrict__ E,
+                                                const double* __restrict__ O,
+                                                const double (&v)[M], double (&o)[M]) {
+  constexpr int H = M / 2;
+  double u[H], w[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    u[i] = v[i] + v[M - 1 - i];
+    w[i] = v[i] - v[M - 1 - i];
+  }
+#pragma unroll
+  for (int r = 0; r < H; ++r) {
+    o[r] = __ldg(E + r) * u[0];
+    o[H + r] = __ldg(O + r) * w[0];
+  }
+#pragma unroll
+  for (int k = 1; k < H; ++k) {
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+      o[r] = fma(__ldg(E + k * H + r), u[k], o[r]);
+      o[H + r] = fma(__ldg(O + k * H + r), w[k], o[H + r]);
+    }
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void matvec_eo_bwd_g(const double* __restrict__ Et,
+                                                const double* __restrict__ Ot,
+                                                const double (&v)[M], double (&o)[M]) {
+  constexpr int H = M / 2;
+  double e[H], q[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    e[i] = __ldg(Et + i) * v[0];
+    q[i] = __ldg(Ot + i) * v[H];
+  }
+#pragma unroll
+  for (int k = 1; k < H; ++k) {
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      e[i] = fma(__ldg(Et + k * H + i), v[k], e[i]);
+      q[i] = fma(__ldg(Ot + k * H + i), v[H + k], q[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    o[i] = e[i] + q[i];
+    o[M - 1 - i] = e[i] - q[i];
+  }
+}
+
+template <int M, bool FWD>
+__device__ __forceinline__ void fdmg_matvec(const FdmgParams& p, int digit, const double (&v)[M],
+                                            double (&o)[M]) {
+  constexpr int HH = (M / 2) * (M / 2);
+  if (p.eo && digit == 0) {
+    if (FWD) matvec_eo_fwd_g<M>(p.eo, p.eo + HH, v, o);
+    else matvec_eo_bwd_g<M>(p.eo + 2 * HH, p.eo + 3 * HH, v, o);
+    return;
+  }
+  matvec_g<M>((FWD ? p.z : p.zt) + (int64_t)digit * M * M, v, o);
 }
 
 template <int D, int M, bool PATCH>
@@ -105,14 +173,13 @@ fdmg_kernel(const FdmgParams p) {
     // forward contractions with Z^T along 0 .. D-1
 #pragma unroll 1
     for (int t = 0; t < D; ++t) {
-      const double* S = p.z + (int64_t)digit[t] * M * M;
       const int ss = sstride(t);
       for (int f = tid; f < F; f += NT) {
         const int sb = sbase(t, f);
         double v[M], o[M];
 #pragma unroll
         for (int k = 0; k < M; ++k) v[k] = T[sb + k * ss];
-        matvec_g<M>(S, v, o);
+        fdmg_matvec<M, true>(p, digit[t], v, o);
         if (t == D - 1) {
           // scale by 1 / (lambda_1 + .. + lambda_d) on the last forward pass
           const int a = (D == 3) ? f % M : f, b = (D == 3) ? f / M : 0;
@@ -130,14 +197,13 @@ fdmg_kernel(const FdmgParams p) {
     // backward contractions with Z along D-1 .. 0
 #pragma unroll 1
     for (int t = D - 1; t >= 0; --t) {
-      const double* S = p.zt + (int64_t)digit[t] * M * M;
       const int ss = sstride(t);
       for (int f = tid; f < F; f += NT) {
         const int sb = sbase(t, f);
         double v[M], o[M];
 #pragma unroll
         for (int k = 0; k < M; ++k) v[k] = T[sb + k * ss];
-        matvec_g<M>(S, v, o);
+        fdmg_matvec<M, false>(p, digit[t], v, o);
 #pragma unroll
         for (int k = 0; k < M; ++k) T[sb + k * ss] = o[k];
       }

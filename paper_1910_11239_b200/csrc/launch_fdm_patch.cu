@@ -22,6 +22,7 @@ static int launch_fdmg(const FdmArgs& q, cudaStream_t st) {
   p.invsum = q.invsum;
   p.z = q.zd;
   p.zt = q.ztd;
+  p.eo = q.eod;  // null when the level was built without the even/odd tables
   p.omega = q.omega;
   p.atomic = q.atomic;
   p.packed = q.packed;
