@@ -83,6 +83,8 @@ def _single_run(dims, k, kind, omega, steps, x0, b):
     ((8, 8, 12), 5, "avs", 3, 2),
     ((5, 6, 8), 3, "acs", 4, 2),
     ((7, 4, 16), 1, "avs", 8, 1),
+    ((3, 2, 8), 8, "avs", 2, 1),   # degree-8 patches: the generic kernel on windowed levels
+    ((2, 3, 12), 9, "avs", 3, 2),
 ])
 def test_emulated_slabs_equal_single_gpu_and_oracle(dims, k, kind, world, steps, avs_atomic):
     omega = 0.25 if kind == "avs" else 0.7
