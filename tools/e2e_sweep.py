@@ -19,11 +19,14 @@ import paper_1910_11239_b200 as dg  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--layers", default="2,4,8,16")
 ap.add_argument("--steps", type=int, default=10)
+ap.add_argument("--config", type=int, default=5, help="BASELINE config (additive kinds: 2, 4, 5)")
 a = ap.parse_args()
-lvl = dg.build_hierarchy(3, 64, 0).levels[0]
-basis = dg.Basis1D.make(5)
+from bench import CONFIGS  # noqa: E402
+c = CONFIGS[a.config]
+lvl = dg.build_hierarchy(c["d"], c["nc"], 0).levels[0]
+basis = dg.Basis1D.make(c["k"])
 ctx = dg.make_context(lvl, basis)
-sm = dg.make_level_smoother(ctx, basis, dg.SmootherConfig(kind="avs", omega=0.25))
+sm = dg.make_level_smoother(ctx, basis, dg.SmootherConfig(kind=c["kind"], omega=c["omega"]))
 n = ctx.ndofs
 xh = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, n)).pin_memory()
 bh = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, n)).pin_memory()
