@@ -343,3 +343,44 @@ def test_compute_rhs_matches_reference(name):
     got = dgop.compute_rhs(ctx, rhs_f, rhs_g)
     assert got.shape == (ctx.ndofs,)
     assert rel(got, G[name + "/rhs"]) <= 1e-13
+
+
+@pytest.mark.parametrize("d,nc,lv,k,kind,om", [(3, 2, 2, 3, "avs", 0.125), (2, 4, 2, 4, "acs", 0.7),
+                                               (3, 2, 2, 2, "mvs", 1.0), (1, 3, 3, 3, "avs", 0.5)])
+def test_vcycle_zero_guess_shortcut_is_exact(d, nc, lv, k, kind, om, monkeypatch):
+    """The first pre-smoothing step of a V-cycle level starts from x = 0, where
+    r = b - A 0 = b bit for bit: the additive kinds skip that residual launch
+    (`LevelSmoother.smooth_from_zero`).  Same cycle as without the shortcut:
+    bitwise for ACS (and MVS, which takes the ordinary step), to rounding for
+    AVS, whose one-launch path sums a DoF's updates in arbitrary order."""
+    cfg = dg.SmootherConfig(kind=kind, omega=om, m_pre=2, m_post=1)
+    out = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv("DGB_ZERO_GUESS", v)
+        _, ctxs, cyc = stack(d, nc, lv, k, smoother=cfg)
+        b = torch.from_numpy(useed(ctxs[-1].ndofs, 0)).cuda()
+        out[v] = cyc.apply(b, torch.empty_like(b)).cpu().numpy()
+    if kind == "avs":
+        assert rel(out["1"], out["0"]) <= 1e-14
+    else:
+        assert np.array_equal(out["0"], out["1"])
+    # and a single step: smooth_from_zero == smooth on a zero vector
+    ctx = ctxs[-1]
+    sm = cyc.smoothers[len(ctxs) - 1]
+    x1 = torch.zeros(ctx.ndofs, dtype=torch.float64, device="cuda")
+    x2 = torch.zeros_like(x1)
+    monkeypatch.setenv("DGB_ZERO_GUESS", "1")
+    sm.smooth_from_zero(x1, b)
+    sm.smooth(x2, b)
+    if kind == "avs":
+        assert float((x1 - x2).norm() / x2.norm()) <= 1e-14
+    else:
+        assert torch.equal(x1, x2)
+    # with the deterministic AVS order requested the shortcut steps aside
+    if kind == "avs":
+        monkeypatch.setenv("DGB_AVS_ATOMIC", "0")
+        x3 = torch.zeros_like(x1)
+        x4 = torch.zeros_like(x1)
+        sm.smooth_from_zero(x3, b)
+        sm.smooth(x4, b)
+        assert torch.equal(x3, x4)
