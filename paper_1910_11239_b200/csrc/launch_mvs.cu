@@ -13,10 +13,8 @@ template <int N>
 static int launch_mvs(const ResArgs& ra, const FdmArgs& fa, const HostRes& h, const double* hz,
                       const double* hzt, const double* heo, cudaStream_t st) {
   if (fa.count <= 0) return DG_OK;
-  constexpr int M = 2 * N;
   using SH = MvsShape<N>;
-  // static: 20 KB of tables, filled once per call site and copied into the launch
-  MvsParams<N> P;
+  MvsParams<N> P;  // ~22 KB of tables and scalars in the kernel parameter space
   Res2Params<3, N>& p = P.res;
   p.x = ra.x;
   p.b = ra.b;
@@ -59,7 +57,6 @@ static int launch_mvs(const ResArgs& ra, const FdmArgs& fa, const HostRes& h, co
   }
   k<<<(unsigned)fa.count, SH::NT, smem, st>>>(P);
   DG_CUDA(cudaGetLastError());
-  (void)M;
   return DG_OK;
 }
 
