@@ -229,4 +229,86 @@ fdmg_kernel(const FdmgParams p) {
   }
 }
 
+// 2D: a patch has only m <= 32 fibers per direction, so one warp owns one
+// patch (lane = fiber, __syncwarp between the passes) and a CTA of 8 warps
+// works on 8 patches at once, each with its own padded tensor in shared
+// memory (m (m+1) doubles).  Same passes and arithmetic as fdmg_kernel<2, m>.
+constexpr int kFdmg2Warps = 8;
+
+template <int M, bool PATCH>
+__global__ void __launch_bounds__(32 * kFdmg2Warps)
+fdmg2_warp_kernel(const FdmgParams p) {
+  static_assert(M % 2 == 0 && M <= 32, "one fiber per lane");
+  constexpr int D = 2;
+  constexpr int N = PATCH ? M / 2 : M;
+  constexpr int NEc = N * N, NE = M * M;
+  constexpr int SLOTS = PATCH ? 4 : 1;
+  constexpr int P = M + 1;
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* T = sm + warp * (P * M);
+  const int64_t nw = (int64_t)gridDim.x * kFdmg2Warps;
+  for (int64_t idx = (int64_t)blockIdx.x * kFdmg2Warps + warp; idx < p.count; idx += nw) {
+    int digit[3] = {0, 0, 0}, base[3] = {0, 0, 0};
+    subdomain_info<D, PATCH>(p.geo, p.list ? p.list[idx] : (int)(p.start + idx), p.packed != 0,
+                             digit, base);
+    const int cls = digit[1] * 4 + digit[0];
+    // gather: row w of cell slot -> T[(s1 N + w) P + s0 N ..]
+    for (int rr = lane; rr < SLOTS * N; rr += 32) {
+      const int slot = rr / N, w = rr - slot * N;
+      const int s0 = slot & 1, s1 = (slot >> 1) & 1;
+      int c[3] = {base[0] + s0, base[1] + s1, 0};
+      const double* src = p.r + (int64_t)cell_local<D>(p.geo, c) * NEc + w * N;
+      double* dst = T + s0 * N + P * (s1 * N + w);
+#pragma unroll 4
+      for (int i = 0; i < N; ++i) dst[i] = __ldg(src + i);
+    }
+    __syncwarp();
+    double v[M], o[M];
+    if (lane < M) {  // Z^T along direction 0: fiber = row `lane`
+#pragma unroll
+      for (int k = 0; k < M; ++k) v[k] = T[lane * P + k];
+      fdmg_matvec<M, true>(p, digit[0], v, o);
+#pragma unroll
+      for (int k = 0; k < M; ++k) T[lane * P + k] = o[k];
+    }
+    __syncwarp();
+    if (lane < M) {  // Z^T along direction 1, 1 / (lambda_0 + lambda_1), Z along direction 1
+#pragma unroll
+      for (int k = 0; k < M; ++k) v[k] = T[lane + k * P];
+      fdmg_matvec<M, true>(p, digit[1], v, o);
+      const double* inv = p.invsum + (int64_t)cls * NE + lane;
+#pragma unroll
+      for (int k = 0; k < M; ++k) o[k] *= __ldg(inv + k * M);
+      fdmg_matvec<M, false>(p, digit[1], o, v);
+#pragma unroll
+      for (int k = 0; k < M; ++k) T[lane + k * P] = v[k];
+    }
+    __syncwarp();
+    if (lane < M) {  // Z along direction 0
+#pragma unroll
+      for (int k = 0; k < M; ++k) v[k] = T[lane * P + k];
+      fdmg_matvec<M, false>(p, digit[0], v, o);
+#pragma unroll
+      for (int k = 0; k < M; ++k) T[lane * P + k] = o[k];
+    }
+    __syncwarp();
+    for (int rr = lane; rr < SLOTS * N; rr += 32) {
+      const int slot = rr / N, w = rr - slot * N;
+      const int s0 = slot & 1, s1 = (slot >> 1) & 1;
+      int c[3] = {base[0] + s0, base[1] + s1, 0};
+      double* dst = p.x + (int64_t)cell_local<D>(p.geo, c) * NEc + w * N;
+      const double* src = T + s0 * N + P * (s1 * N + w);
+      if (p.atomic) {
+#pragma unroll 4
+        for (int i = 0; i < N; ++i) atomicAdd(dst + i, p.omega * src[i]);
+      } else {
+#pragma unroll 4
+        for (int i = 0; i < N; ++i) dst[i] = xupd(dst[i], p.omega, src[i]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace dgb

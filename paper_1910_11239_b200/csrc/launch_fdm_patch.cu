@@ -27,6 +27,24 @@ static int launch_fdmg(const FdmArgs& q, cudaStream_t st) {
   p.atomic = q.atomic;
   p.packed = q.packed;
   p.geo = q.geo;
+  if constexpr (D == 2 && M <= 32) {
+    // 2D: one warp per patch, 8 patches per CTA (fdmg2_warp_kernel)
+    if (env_int("DGB_FDMG2_WARP", 1)) {
+      p.pitch = M + 1;
+      p.scratch = nullptr;
+      const size_t smem2 = sizeof(double) * (size_t)kFdmg2Warps * (M + 1) * M;
+      auto k2 = fdmg2_warp_kernel<M, PATCH>;
+      static bool attr2 = false;
+      if (!attr2 && smem2 > 48 * 1024) {
+        DG_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        attr2 = true;
+      }
+      const int64_t ctas = (q.count + kFdmg2Warps - 1) / kFdmg2Warps;
+      k2<<<(unsigned)std::min<int64_t>(ctas, 1 << 20), 32 * kFdmg2Warps, smem2, st>>>(p);
+      DG_CUDA(cudaGetLastError());
+      return DG_OK;
+    }
+  }
   // shared memory with an odd pitch while the tensor fits, else the level's
   // global scratch (one dense tensor per resident CTA)
   constexpr int64_t rows = (D == 3) ? (int64_t)M * M : M;
